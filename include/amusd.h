@@ -1,0 +1,187 @@
+/*
+ * amusd.h -- C-ABI of the B200-native AMUSD draft/verify decode path.
+ *
+ * The reference (pkg/src/specdec) is pure Python with two duck-typed plug-in
+ * points and no FFI.  This header is the boundary a
+ * maintainer binds (ctypes stub in INTEGRATION.md); every entry point names the
+ * reference interface it replaces.  Conventions:
+ *   - plain pointers and sizes only; no torch types;
+ *   - all DEVICE memory (weights, KV cache, activations, mailbox, trace rings,
+ *     canonical table) is allocated by the caller and passed in; the library
+ *     never allocates device memory.  Host-side handles (graphs, TMA
+ *     descriptors) are owned by the opaque amusd_model / amusd_session;
+ *   - every function returns an amusd_status; amusd_last_error() gives text;
+ *   - streams are cudaStream_t passed as void*.
+ */
+#ifndef AMUSD_H
+#define AMUSD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AMUSD_ABI_VERSION 1
+#define AMUSD_KMAX 16          /* rows in one forward: verify window + pending */
+#define AMUSD_MAX_LAYERS 128
+
+/* Status codes; the Python wrapper maps them onto the reference hierarchy
+ * (errors.py:4-29). */
+typedef enum {
+  AMUSD_OK = 0,
+  AMUSD_ERR_INVALID_INPUT = 1,    /* InvalidInputError       errors.py:8  */
+  AMUSD_ERR_INVALID_ROLLBACK = 2, /* InvalidRollbackError    errors.py:12 */
+  AMUSD_ERR_PROTOCOL = 3,         /* ProtocolViolationError  errors.py:16 */
+  AMUSD_ERR_CUDA = 4,             /* SpecDecError (runtime)  errors.py:4  */
+  AMUSD_ERR_UNSUPPORTED = 5       /* SpecDecError                          */
+} amusd_status;
+
+typedef enum { AMUSD_F32 = 0, AMUSD_BF16 = 1 } amusd_dtype;
+
+/* Engines (engines.py:279-301, 534-561). */
+typedef enum {
+  AMUSD_ENGINE_AUTOREGRESSIVE = 0, /* decode_autoregressive    engines.py:279 */
+  AMUSD_ENGINE_SYNC = 1,           /* decode_speculative_sync  engines.py:290 */
+  AMUSD_ENGINE_ASYNC = 2,          /* decode_speculative_async engines.py:534 */
+  AMUSD_ENGINE_ASYNC_DRAFT = 3,    /* draft loop only (draft GPU of a split pair) */
+  AMUSD_ENGINE_ASYNC_VERIFY = 4    /* verify loop only (verify GPU of a split pair) */
+} amusd_engine;
+
+/* Draft agreement coin (models.py:271-314). */
+typedef enum {
+  AMUSD_COIN_NONE = 0,  /* draft emits its own greedy token                       */
+  AMUSD_COIN_SELF = 1,  /* agreed = the draft's own greedy token (coin on its prefix) */
+  AMUSD_COIN_CANON = 2  /* agreed = canonical verify token while on the canonical
+                           path (transformer pairs)       */
+} amusd_coin_mode;
+
+typedef struct amusd_model amusd_model;
+typedef struct amusd_session amusd_session;
+
+/* ---------------------------------------------------------------- models */
+
+/* Llama-style decoder shape (builder-defined). */
+typedef struct {
+  int vocab, d_model, n_layers, n_heads, n_kv_heads, head_dim, ffn;
+  int max_seq;       /* KV capacity in tokens                         */
+  int dtype;         /* amusd_dtype of weights and KV cache           */
+  int eos_token;
+  int exclude_eos;   /* mask eos from the argmax (models.py:256-261)  */
+  float norm_eps;
+  int use_tensor_cores; /* bf16 only: tcgen05 GEMMs for >2-row forwards */
+} amusd_tf_config;
+
+/* Device pointers, row-major [out][in]; dtype per config (norms are always
+ * the model dtype; rope tables are fp32 [max_seq][head_dim/2]). */
+typedef struct {
+  const void* embed;       /* [vocab][d]                     */
+  const void* lm_head;     /* [vocab][d]; == embed when tied  */
+  const void* final_norm;  /* [d]                             */
+  const float* rope_cos;
+  const float* rope_sin;
+  const void* attn_norm[AMUSD_MAX_LAYERS]; /* [d]                       */
+  const void* wqkv[AMUSD_MAX_LAYERS];      /* [(H+2*KV)*hd][d]          */
+  const void* wo[AMUSD_MAX_LAYERS];        /* [d][H*hd]                 */
+  const void* mlp_norm[AMUSD_MAX_LAYERS];  /* [d]                       */
+  const void* wgate[AMUSD_MAX_LAYERS];     /* [ffn][d]                  */
+  const void* wup[AMUSD_MAX_LAYERS];       /* [ffn][d]                  */
+  const void* wdown[AMUSD_MAX_LAYERS];     /* [d][ffn]                  */
+} amusd_tf_weights;
+
+/* Bytes of device state (KV cache + activations + sequence state). */
+size_t amusd_tf_state_bytes(const amusd_tf_config* cfg);
+int amusd_tf_create(amusd_model** out, const amusd_tf_config* cfg, const amusd_tf_weights* w,
+                    void* state, size_t state_bytes);
+
+/* splitmix64 hash-chain model (models.py:203-268): the device test double (K7).
+ * agreement_rho < 0: HashChainModel; in [0,1]: AgreementDraftModel whose
+ * forward applies the prefix-keyed agreement coin (models.py:271-314). */
+size_t amusd_hash_state_bytes(int max_seq);
+int amusd_hash_create(amusd_model** out, uint64_t seed, int vocab, int eos_token, int exclude_eos,
+                      double agreement_rho, int max_seq, void* state, size_t state_bytes);
+
+int amusd_model_destroy(amusd_model* m);
+
+/* MockModel interface (models.py:85-200): synchronous on `stream`, host token
+ * buffers.  Used by the parity path; the decode loops below never call it. */
+int amusd_init_state(amusd_model* m, const int32_t* prompt, int n, void* stream);       /* models.py:109 */
+int amusd_next_token(amusd_model* m, int32_t* out, void* stream);                        /* models.py:120 */
+int amusd_advance(amusd_model* m, const int32_t* tokens, int n, void* stream);            /* models.py:125 */
+int amusd_rollback(amusd_model* m, int position, void* stream);                           /* models.py:133 */
+int amusd_verify_tokens(amusd_model* m, const int32_t* cands, int n, int32_t* preds,
+                        void* stream);                                                    /* models.py:151 */
+int amusd_prefix_length(amusd_model* m, int* out);                                        /* models.py:72  */
+/* Raw last-row logits of the most recent forward (debug/parity; fp32, vocab entries). */
+int amusd_last_logits(amusd_model* m, float* out, int rows, void* stream);
+
+/* ------------------------------------------------------------- sessions */
+
+typedef struct {
+  int prompt_len;
+  int max_new_tokens;     /* DecodeConfig.max_new_tokens  engines.py:61 */
+  int draft_window_k;     /* DecodeConfig.draft_window_k  engines.py:62 */
+  int max_draft_lead;     /* DecodeConfig.max_draft_lead  engines.py:63 (0 = None) */
+  int max_window;         /* verify rows cap, <= AMUSD_KMAX            */
+  int coin_mode;          /* amusd_coin_mode                           */
+  double rho;             /* agreement probability                      */
+  uint64_t coin_seed;     /* hash-chain seed of the coin                */
+  const int32_t* canon;   /* device [canon_len] absolute tokens (COIN_CANON) */
+  int canon_len;
+  int trace_cap;          /* events per actor ring                      */
+  int jitter_ns;          /* device-side poll jitter (ThreadExecutor.poll_jitter_ms analog) */
+  uint64_t jitter_seed;
+} amusd_session_desc;
+
+/* Mailbox = SharedDecodeState (coordination.py:114-275) in HBM. */
+int amusd_mailbox_capacity(const amusd_session_desc* d); /* tokens per D/V buffer */
+size_t amusd_mailbox_bytes(int capacity_tokens);
+size_t amusd_session_bytes(const amusd_session_desc* d);
+
+/* draft or verify may be NULL for one half of a split pair.  mb_peer is the
+ * peer GPU's mailbox mapped over NVLink (NULL when co-located). */
+int amusd_session_create(amusd_session** out, amusd_model* draft, amusd_model* verify,
+                         const amusd_session_desc* d, void* mem, size_t mem_bytes,
+                         void* mb_local, void* mb_peer);
+int amusd_session_destroy(amusd_session* s);
+
+/* Reset the mailbox, coin chain and trace rings for a fresh run; the models
+ * must already hold init_state(prompt).  Prompt is a host buffer. */
+int amusd_session_reset(amusd_session* s, const int32_t* prompt, int n, void* stream);
+
+/* Launch one engine as device-driven CUDA graphs (conditional WHILE loops):
+ * no host sync inside; returns after enqueueing. ASYNC uses both streams. */
+int amusd_session_launch(amusd_session* s, int engine, void* verify_stream, void* draft_stream);
+
+/* Verified stream V and counters after a run (host buffers). */
+typedef struct {
+  int p_v, p_d, complete, error;
+  int verify_steps, rollbacks, drafted, acks;
+  int n_draft_events, n_verify_events;
+} amusd_run_info;
+int amusd_session_info(amusd_session* s, amusd_run_info* info, int32_t* V, int v_cap, void* stream);
+
+/* Trace events (metrics.py:60-72): kind 0 draft_token, 1 verify_accept,
+ * 2 verify_correct, 3 rollback; times in ns from %globaltimer. */
+typedef struct {
+  int64_t t_ns;
+  int64_t busy_ns;
+  int32_t kind, pos_lo, pos_hi, draft_accepted;
+} amusd_trace_event;
+int amusd_session_trace(amusd_session* s, int actor /*0 draft, 1 verify*/, amusd_trace_event* out,
+                        int cap, int* n, void* stream);
+
+/* ---------------------------------------------------------------- misc */
+int amusd_abi_version(void);
+const char* amusd_last_error(void);
+/* Number of kernels one step of `engine` launches (gpu_launches accounting). */
+int amusd_session_kernels_per_step(amusd_session* s, int engine, int* draft_step, int* verify_step);
+/* Device-side deterministic weight fill: w[i] = scale * u(splitmix64(seed + i)),
+ * u uniform in [-1,1) -- used for synthetic bf16/fp32 weights. */
+int amusd_fill_uniform(void* dst, int dtype, size_t n, uint64_t seed, float scale, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AMUSD_H */

@@ -1,0 +1,727 @@
+// api.cu -- the extern "C" boundary declared in include/amusd.h.
+//
+// Host side of the path: model handles (MockModel, models.py:85-200),
+// sessions (SharedDecodeState + executor, coordination.py:114-275,
+// engines.py:409-561) and the CUDA-graph construction that turns each engine
+// into a device-driven WHILE loop.  No device allocation happens here.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/amusd.h"
+#include "common.cuh"
+#include "internal.h"
+#include "protocol.h"
+#include "transformer.h"
+
+using namespace amusd;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                          \
+  do {                                                                                       \
+    cudaError_t e__ = (x);                                                                   \
+    if (e__ != cudaSuccess)                                                                  \
+      return fail(AMUSD_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e__));        \
+  } while (0)
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct Carver {
+  char* base;
+  size_t off = 0;
+  explicit Carver(void* b) : base((char*)b) {}
+  template <typename T>
+  T* take(size_t count) {
+    off = align_up(off, 256);
+    T* p = base ? (T*)(base + off) : nullptr;
+    off += sizeof(T) * count;
+    return p;
+  }
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------- model
+struct amusd_model {
+  int kind = 0;  // 0 transformer, 1 hash chain
+  int vocab = 0, eos = 0, exclude_eos = 0, max_seq = 0;
+  // device state
+  SeqHdr* seq = nullptr;
+  int* tok = nullptr;
+  StepCtl* api_ctl = nullptr;
+  // host mirror of the sequence (parity API)
+  int prompt_len = 0, len = 0, kv_len = 0;
+  bool pred_valid = false;
+  int pred = 0;
+  bool dirty = false;  // device loops advanced the state since the last sync
+  std::vector<int> htok;
+  // hash chain
+  unsigned long long seed = 0;
+  unsigned long long* chain = nullptr;
+  bool agree = false, agree_always = false;
+  unsigned long long agree_thr = 0;
+  // transformer
+  amusd_tf_config cfg{};
+  amusd_tf_weights w{};
+  void *kc = nullptr, *vc = nullptr;
+  float *h = nullptr, *qkv = nullptr, *attn = nullptr, *act = nullptr, *logits = nullptr;
+  unsigned long long* part = nullptr;
+  int lm_grid = 0;
+  size_t kv_layer_elems = 0;
+  int last_rows = 0;
+};
+
+static size_t tf_carve(const amusd_tf_config* c, void* base, amusd_model* m) {
+  Carver cv(base);
+  const size_t wsz = c->dtype == AMUSD_BF16 ? 2 : 4;
+  const int ncols = (c->n_heads + 2 * c->n_kv_heads) * c->head_dim;
+  const size_t kv = (size_t)c->n_layers * c->n_kv_heads * c->max_seq * c->head_dim;
+  const int lm_grid = gemv_grid(c->vocab, 2);
+  SeqHdr* seq = cv.take<SeqHdr>(1);
+  int* tok = cv.take<int>(c->max_seq + 1);
+  StepCtl* ctl = cv.take<StepCtl>(1);
+  char* kc = cv.take<char>(kv * wsz);
+  char* vc = cv.take<char>(kv * wsz);
+  float* h = cv.take<float>((size_t)KMAX * c->d_model);
+  float* qkv = cv.take<float>((size_t)KMAX * ncols);
+  float* attn = cv.take<float>((size_t)KMAX * c->n_heads * c->head_dim);
+  float* act = cv.take<float>((size_t)KMAX * c->ffn);
+  unsigned long long* part = cv.take<unsigned long long>((size_t)KMAX * lm_grid);
+  float* logits = cv.take<float>((size_t)KMAX * c->vocab);
+  if (m) {
+    m->seq = seq; m->tok = tok; m->api_ctl = ctl; m->kc = kc; m->vc = vc; m->h = h; m->qkv = qkv;
+    m->attn = attn; m->act = act; m->part = part; m->logits = logits; m->lm_grid = lm_grid;
+    m->kv_layer_elems = (size_t)c->n_kv_heads * c->max_seq * c->head_dim;
+  }
+  return align_up(cv.off, 256);
+}
+
+static size_t hash_carve(int max_seq, void* base, amusd_model* m) {
+  Carver cv(base);
+  SeqHdr* seq = cv.take<SeqHdr>(1);
+  int* tok = cv.take<int>(max_seq + 1);
+  StepCtl* ctl = cv.take<StepCtl>(1);
+  unsigned long long* chain = cv.take<unsigned long long>(max_seq + 2);
+  if (m) { m->seq = seq; m->tok = tok; m->api_ctl = ctl; m->chain = chain; }
+  return align_up(cv.off, 256);
+}
+
+// Enqueue one forward of `m` driven by control block `ctl` (rows <= nr).
+static int model_forward(amusd_model* m, StepCtl* ctl, int nr, cudaStream_t st, bool pdl, bool want_logits) {
+  if (m->kind == 1) {
+    CUDA_TRY(launch_hash_forward(ctl, m->chain, m->vocab, m->eos, m->exclude_eos, m->agree, m->agree_always, m->agree_thr, st));
+    return AMUSD_OK;
+  }
+  const amusd_tf_config& c = m->cfg;
+  const int dt = c.dtype;
+  const size_t wsz = dt == AMUSD_BF16 ? 2 : 4;
+  const int d = c.d_model, hd = c.head_dim, H = c.n_heads, KV = c.n_kv_heads;
+  const int ncols = (H + 2 * KV) * hd;
+  CUDA_TRY(launch_embed(dt, ctl, m->w.embed, m->h, d, st, pdl));
+  for (int l = 0; l < c.n_layers; ++l) {
+    GemvArgs g{};
+    g.ctl = ctl; g.eps = c.norm_eps; g.eos = c.eos_token; g.exclude_eos = c.exclude_eos;
+    // QKV (attention RMSNorm fused)
+    g.x = m->h; g.ldx = d; g.gamma = m->w.attn_norm[l]; g.W = m->w.wqkv[l]; g.N = ncols; g.K = d;
+    g.kc = gemv_kc(nr, d); g.out = m->qkv; g.ldo = ncols;
+    CUDA_TRY(launch_gemv(nr, dt, kEpiStore, g, st, pdl));
+    // attention (RoPE + KV append fused)
+    AttnArgs at{};
+    at.ctl = ctl; at.qkv = m->qkv;
+    at.kc = (char*)m->kc + (size_t)l * m->kv_layer_elems * wsz;
+    at.vc = (char*)m->vc + (size_t)l * m->kv_layer_elems * wsz;
+    at.cos = m->w.rope_cos; at.sin = m->w.rope_sin; at.out = m->attn; at.ldo = H * hd;
+    at.H = H; at.KV = KV; at.hd = hd; at.S = c.max_seq; at.scale = 1.0f / sqrtf((float)hd);
+    CUDA_TRY(launch_attention(dt, at, st, pdl));
+    // O projection + residual
+    g.x = m->attn; g.ldx = H * hd; g.gamma = nullptr; g.W = m->w.wo[l]; g.N = d; g.K = H * hd;
+    g.kc = gemv_kc(nr, H * hd); g.out = m->h; g.ldo = d;
+    CUDA_TRY(launch_gemv(nr, dt, kEpiResid, g, st, pdl));
+    // gate/up (MLP RMSNorm + SiLU*mul fused)
+    g.x = m->h; g.ldx = d; g.gamma = m->w.mlp_norm[l]; g.W = m->w.wgate[l]; g.W2 = m->w.wup[l];
+    g.N = c.ffn; g.K = d; g.kc = gemv_kc(nr, d); g.out = m->act; g.ldo = c.ffn;
+    CUDA_TRY(launch_gemv(nr, dt, kEpiGateUp, g, st, pdl));
+    // down projection + residual
+    g.x = m->act; g.ldx = c.ffn; g.gamma = nullptr; g.W = m->w.wdown[l]; g.W2 = nullptr; g.N = d;
+    g.K = c.ffn; g.kc = gemv_kc(nr, c.ffn); g.out = m->h; g.ldo = d;
+    CUDA_TRY(launch_gemv(nr, dt, kEpiResid, g, st, pdl));
+  }
+  GemvArgs g{};
+  g.ctl = ctl; g.eps = c.norm_eps; g.eos = c.eos_token; g.exclude_eos = c.exclude_eos;
+  g.x = m->h; g.ldx = d; g.gamma = m->w.final_norm; g.W = m->w.lm_head; g.N = c.vocab; g.K = d;
+  g.kc = gemv_kc(nr, d); g.part = m->part; g.logits = want_logits ? m->logits : nullptr;
+  CUDA_TRY(launch_gemv(nr, dt, kEpiArgmax, g, st, pdl));
+  CUDA_TRY(launch_argmax_final(ctl, m->part, m->lm_grid, st, pdl));
+  return AMUSD_OK;
+}
+
+static int model_kernels_per_forward(const amusd_model* m) {
+  return m->kind == 1 ? 1 : 1 + 5 * m->cfg.n_layers + 2;
+}
+
+extern "C" {
+
+int amusd_abi_version(void) { return AMUSD_ABI_VERSION; }
+const char* amusd_last_error(void) { return g_err.c_str(); }
+
+size_t amusd_tf_state_bytes(const amusd_tf_config* cfg) { return cfg ? tf_carve(cfg, nullptr, nullptr) : 0; }
+
+int amusd_tf_create(amusd_model** out, const amusd_tf_config* cfg, const amusd_tf_weights* w, void* state,
+                    size_t state_bytes) {
+  if (!out || !cfg || !w || !state) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  const amusd_tf_config& c = *cfg;
+  if (c.vocab < 2 || c.d_model <= 0 || c.n_layers <= 0 || c.n_layers > AMUSD_MAX_LAYERS || c.n_heads <= 0 ||
+      c.n_kv_heads <= 0 || c.n_heads % c.n_kv_heads || c.head_dim % 8 || c.head_dim > 256 || c.ffn <= 0 ||
+      c.max_seq < 2)
+    return fail(AMUSD_ERR_INVALID_INPUT, "invalid transformer config");
+  if (!(0 <= c.eos_token && c.eos_token < c.vocab))
+    return fail(AMUSD_ERR_INVALID_INPUT, "eos_token out of range");  // models.py:98-101
+  if (c.d_model % 256 || c.ffn % 256 || (c.n_heads * c.head_dim) % 256)
+    return fail(AMUSD_ERR_UNSUPPORTED, "d_model, ffn and n_heads*head_dim must be multiples of 256");
+  if (c.dtype != AMUSD_F32 && c.dtype != AMUSD_BF16) return fail(AMUSD_ERR_INVALID_INPUT, "bad dtype");
+  if (state_bytes < amusd_tf_state_bytes(cfg)) return fail(AMUSD_ERR_INVALID_INPUT, "state buffer too small");
+  if (((size_t)c.max_seq + 2 * KMAX + 1) * sizeof(float) * 1 > 190 * 1024)
+    return fail(AMUSD_ERR_UNSUPPORTED, "max_seq too large for the attention kernel");
+  amusd_model* m = new amusd_model();
+  m->kind = 0;
+  m->cfg = c;
+  m->w = *w;
+  m->vocab = c.vocab;
+  m->eos = c.eos_token;
+  m->exclude_eos = c.exclude_eos;
+  m->max_seq = c.max_seq;
+  tf_carve(cfg, state, m);
+  *out = m;
+  return AMUSD_OK;
+}
+
+size_t amusd_hash_state_bytes(int max_seq) { return hash_carve(max_seq, nullptr, nullptr); }
+
+int amusd_hash_create(amusd_model** out, uint64_t seed, int vocab, int eos, int exclude_eos, double rho,
+                      int max_seq, void* state, size_t state_bytes) {
+  if (!out || !state) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  if (vocab < 2) return fail(AMUSD_ERR_INVALID_INPUT, "vocab_size must be >= 2");  // models.py:96
+  if (!(0 <= eos && eos < vocab)) return fail(AMUSD_ERR_INVALID_INPUT, "eos_token out of range");
+  if (exclude_eos && vocab < 3) return fail(AMUSD_ERR_INVALID_INPUT, "exclude_eos requires vocab_size >= 3");
+  if (max_seq < 2) return fail(AMUSD_ERR_INVALID_INPUT, "max_seq must be >= 2");
+  if (rho > 1.0) return fail(AMUSD_ERR_INVALID_INPUT, "agreement_rho must be in [0, 1]");  // models.py:290
+  if (rho >= 0.0 && rho < 1.0 && vocab - (exclude_eos ? 1 : 0) < 2)
+    return fail(AMUSD_ERR_INVALID_INPUT, "vocabulary too small to hold a disagreeing token alternative");
+  if (state_bytes < amusd_hash_state_bytes(max_seq)) return fail(AMUSD_ERR_INVALID_INPUT, "state buffer too small");
+  amusd_model* m = new amusd_model();
+  m->kind = 1;
+  m->seed = seed;
+  m->vocab = vocab;
+  m->eos = eos;
+  m->exclude_eos = exclude_eos;
+  m->max_seq = max_seq;
+  m->agree = rho >= 0.0;
+  m->agree_always = rho >= 1.0;
+  m->agree_thr = m->agree_always ? ~0ull : (rho >= 0.0 ? (unsigned long long)(rho * 18446744073709551616.0) : 0ull);
+  hash_carve(max_seq, state, m);
+  *out = m;
+  return AMUSD_OK;
+}
+
+int amusd_model_destroy(amusd_model* m) {
+  delete m;
+  return AMUSD_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------- MockModel parity path
+static int sync_from_device(amusd_model* m, cudaStream_t st) {
+  if (!m->dirty) return AMUSD_OK;
+  SeqHdr h;
+  CUDA_TRY(cudaMemcpyAsync(&h, m->seq, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  m->htok.resize(h.len);
+  if (h.len) CUDA_TRY(cudaMemcpyAsync(m->htok.data(), m->tok, sizeof(int) * h.len, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  m->len = h.len;
+  m->kv_len = h.kv_len;
+  m->pred_valid = false;
+  m->dirty = false;
+  return AMUSD_OK;
+}
+
+static int push_header(amusd_model* m, cudaStream_t st) {
+  SeqHdr h{};
+  h.len = m->len;
+  h.kv_len = m->kv_len;
+  h.prompt_len = m->prompt_len;
+  h.cap = m->max_seq;
+  h.pred_valid = 0;
+  CUDA_TRY(cudaMemcpyAsync(m->seq, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  return AMUSD_OK;
+}
+
+// Forward explicit rows (positions pos0..) on the model's API control block;
+// returns the predictions (host) after a stream sync.
+static int api_forward(amusd_model* m, int pos0, const int* rows_tok, int rows, int* preds, cudaStream_t st) {
+  StepCtl c{};
+  c.active = 1;
+  c.rows = rows;
+  c.pos0 = pos0;
+  c.npend = rows;
+  for (int i = 0; i < rows; ++i) c.tok[i] = rows_tok[i];
+  CUDA_TRY(cudaMemcpyAsync(m->api_ctl, &c, sizeof(c), cudaMemcpyHostToDevice, st));
+  int r = model_forward(m, m->api_ctl, rows <= 2 ? 2 : KMAX, st, false, true);
+  if (r) return r;
+  m->last_rows = rows;
+  if (preds) {
+    CUDA_TRY(cudaMemcpyAsync(preds, m->api_ctl->preds, sizeof(int) * rows, cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaGetLastError());
+  return AMUSD_OK;
+}
+
+// Bring the cache up to len-1 (at most `keep` pending tokens stay uncached).
+static int catch_up(amusd_model* m, int keep, cudaStream_t st) {
+  if (m->kv_len >= m->len) m->kv_len = m->len - 1;
+  while (m->len - m->kv_len > keep) {
+    const int rows = std::min(KMAX, m->len - m->kv_len - keep);
+    int r = api_forward(m, m->kv_len, m->htok.data() + m->kv_len, rows, nullptr, st);
+    if (r) return r;
+    m->kv_len += rows;
+  }
+  return AMUSD_OK;
+}
+
+static int validate_tokens(const amusd_model* m, const int32_t* t, int n) {
+  for (int i = 0; i < n; ++i)
+    if (t[i] < 0 || t[i] >= m->vocab)
+      return fail(AMUSD_ERR_INVALID_INPUT, "token " + std::to_string(t[i]) + " out of vocabulary range [0, " +
+                                               std::to_string(m->vocab) + ")");
+  return AMUSD_OK;
+}
+
+extern "C" {
+
+int amusd_init_state(amusd_model* m, const int32_t* prompt, int n, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!m) return fail(AMUSD_ERR_INVALID_INPUT, "null model");
+  if (n <= 0) return fail(AMUSD_ERR_INVALID_INPUT, "prompt must be non-empty");  // models.py:111
+  if (int r = validate_tokens(m, prompt, n)) return r;
+  if (n + 1 > m->max_seq) return fail(AMUSD_ERR_INVALID_INPUT, "prompt exceeds max_seq");
+  m->htok.assign(prompt, prompt + n);
+  m->prompt_len = n;
+  m->len = n;
+  m->kv_len = 0;
+  m->pred_valid = false;
+  m->dirty = false;
+  CUDA_TRY(cudaMemcpyAsync(m->tok, prompt, sizeof(int) * n, cudaMemcpyHostToDevice, st));
+  if (m->kind == 1) CUDA_TRY(launch_hash_seed(m->chain, m->seed, st));
+  if (int r = catch_up(m, 1, st)) return r;
+  if (int r = push_header(m, st)) return r;
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return AMUSD_OK;
+}
+
+int amusd_next_token(amusd_model* m, int32_t* out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!m || !out) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  if (int r = sync_from_device(m, st)) return r;
+  if (m->pred_valid) { *out = m->pred; return AMUSD_OK; }
+  if (int r = catch_up(m, KMAX, st)) return r;
+  const int rows = m->len - m->kv_len;
+  int preds[KMAX];
+  if (int r = api_forward(m, m->kv_len, m->htok.data() + m->kv_len, rows, preds, st)) return r;
+  m->kv_len = m->len;
+  m->pred = preds[rows - 1];
+  m->pred_valid = true;
+  *out = m->pred;
+  return push_header(m, st);
+}
+
+int amusd_advance(amusd_model* m, const int32_t* tokens, int n, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!m) return fail(AMUSD_ERR_INVALID_INPUT, "null model");
+  if (int r = sync_from_device(m, st)) return r;
+  if (n <= 0) return fail(AMUSD_ERR_INVALID_INPUT, "advance requires at least one token");  // models.py:128
+  if (int r = validate_tokens(m, tokens, n)) return r;
+  if (m->len + n + 1 > m->max_seq) return fail(AMUSD_ERR_INVALID_INPUT, "sequence exceeds max_seq");
+  CUDA_TRY(cudaMemcpyAsync(m->tok + m->len, tokens, sizeof(int) * n, cudaMemcpyHostToDevice, st));
+  m->htok.insert(m->htok.end(), tokens, tokens + n);
+  m->len += n;
+  m->pred_valid = false;
+  if (int r = push_header(m, st)) return r;
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return AMUSD_OK;
+}
+
+int amusd_rollback(amusd_model* m, int position, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!m) return fail(AMUSD_ERR_INVALID_INPUT, "null model");
+  if (int r = sync_from_device(m, st)) return r;
+  if (position > m->len)  // models.py:140-147
+    return fail(AMUSD_ERR_INVALID_ROLLBACK, "rollback position " + std::to_string(position) +
+                                                " exceeds prefix length " + std::to_string(m->len));
+  if (position < m->prompt_len)
+    return fail(AMUSD_ERR_INVALID_ROLLBACK, "rollback position " + std::to_string(position) +
+                                                " is below prompt length " + std::to_string(m->prompt_len));
+  if (position == m->len) return AMUSD_OK;
+  m->len = position;
+  m->htok.resize(position);
+  m->kv_len = std::min(m->kv_len, position);  // cache-length truncate, no copy
+  m->pred_valid = false;
+  if (int r = push_header(m, st)) return r;
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return AMUSD_OK;
+}
+
+int amusd_verify_tokens(amusd_model* m, const int32_t* cands, int n, int32_t* preds, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!m || !preds) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  if (int r = sync_from_device(m, st)) return r;
+  if (n <= 0) return fail(AMUSD_ERR_INVALID_INPUT, "verify_tokens requires at least one candidate");
+  if (int r = validate_tokens(m, cands, n)) return r;
+  if (m->len + n + 1 > m->max_seq) return fail(AMUSD_ERR_INVALID_INPUT, "sequence exceeds max_seq");
+  if (int r = catch_up(m, 1, st)) return r;
+  // rows: [pending, c_0 .. c_{n-2}] in chunks of KMAX; chunk i continues at
+  // the positions after chunk i-1 (teacher forcing; cache beyond len is scratch)
+  std::vector<int> rows_tok;
+  rows_tok.push_back(m->htok[m->len - 1]);
+  for (int j = 0; j + 1 < n; ++j) rows_tok.push_back(cands[j]);
+  int pos = m->kv_len, done = 0;
+  int buf[KMAX];
+  while (done < (int)rows_tok.size()) {
+    const int rows = std::min(KMAX, (int)rows_tok.size() - done);
+    if (int r = api_forward(m, pos, rows_tok.data() + done, rows, buf, st)) return r;
+    for (int i = 0; i < rows; ++i) preds[done + i] = buf[i];
+    done += rows;
+    pos += rows;
+  }
+  m->kv_len = m->len;
+  m->pred = preds[0];
+  m->pred_valid = true;
+  return push_header(m, st);
+}
+
+int amusd_prefix_length(amusd_model* m, int* out) {
+  if (!m || !out) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  if (int r = sync_from_device(m, 0)) return r;
+  *out = m->len;
+  return AMUSD_OK;
+}
+
+int amusd_last_logits(amusd_model* m, float* out, int rows, void* stream) {
+  if (!m || !out) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  if (m->kind != 0) return fail(AMUSD_ERR_UNSUPPORTED, "logits exist only for transformer models");
+  rows = std::min(rows, m->last_rows);
+  CUDA_TRY(cudaMemcpyAsync(out, m->logits, sizeof(float) * (size_t)rows * m->vocab, cudaMemcpyDeviceToHost,
+                           (cudaStream_t)stream));
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  return AMUSD_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ session
+struct amusd_session {
+  amusd_model* draft = nullptr;
+  amusd_model* verify = nullptr;
+  amusd_session_desc d{};
+  int cap = 0;
+  MailboxHdr* mb_local = nullptr;
+  MailboxHdr* mb_peer = nullptr;
+  StepCtl* dctl = nullptr;
+  StepCtl* vctl = nullptr;
+  TraceDev dtrace{}, vtrace{};
+  CoinDev coin{};
+  int* prompt_dev = nullptr;
+  int prompt_cap = 0;
+  cudaStream_t capture = nullptr;
+  cudaGraphExec_t exec[5][2] = {};
+  bool use_pdl = true;
+};
+
+static int mailbox_cap(const amusd_session_desc* d) { return d->max_new_tokens + 4 * KMAX + 64; }
+
+static size_t session_carve(const amusd_session_desc* d, int coin_cap, int prompt_cap, void* base,
+                            amusd_session* s) {
+  Carver cv(base);
+  StepCtl* dctl = cv.take<StepCtl>(1);
+  StepCtl* vctl = cv.take<StepCtl>(1);
+  amusd_trace_event* dev = cv.take<amusd_trace_event>(d->trace_cap);
+  amusd_trace_event* vev = cv.take<amusd_trace_event>(d->trace_cap);
+  int* counts = cv.take<int>(2);
+  unsigned long long* hash = cv.take<unsigned long long>(coin_cap + 2);
+  unsigned char* onpath = cv.take<unsigned char>(coin_cap + 2);
+  int* prompt = cv.take<int>(prompt_cap);
+  if (s) {
+    s->dctl = dctl; s->vctl = vctl;
+    s->dtrace = TraceDev{dev, counts, d->trace_cap};
+    s->vtrace = TraceDev{vev, counts + 1, d->trace_cap};
+    s->coin.hash = hash; s->coin.onpath = onpath;
+    s->prompt_dev = prompt; s->prompt_cap = prompt_cap;
+  }
+  return align_up(cv.off, 256);
+}
+
+static int session_max_seq(const amusd_session_desc* d) { return d->prompt_len + mailbox_cap(d) + 8; }
+
+static ProtoArgs make_args(amusd_session* s) {
+  ProtoArgs a{};
+  a.mb_local = s->mb_local;
+  a.mb_peer = s->mb_peer;
+  a.cap = s->cap;
+  a.P = s->d.prompt_len;
+  a.N = s->d.max_new_tokens;
+  a.lead = s->d.max_draft_lead;
+  a.max_window = s->d.max_window;
+  a.k = s->d.draft_window_k;
+  if (s->draft) { a.dseq = s->draft->seq; a.dtok = s->draft->tok; }
+  if (s->verify) { a.vseq = s->verify->seq; a.vtok = s->verify->tok; a.vocab_v = s->verify->vocab; a.eos_v = s->verify->eos; }
+  a.dctl = s->dctl;
+  a.vctl = s->vctl;
+  a.dtrace = s->dtrace;
+  a.vtrace = s->vtrace;
+  a.coin = s->coin;
+  a.jitter_ns = s->d.jitter_ns;
+  a.jitter_seed = s->d.jitter_seed;
+  return a;
+}
+
+extern "C" {
+
+size_t amusd_mailbox_bytes(int capacity_tokens) { return mailbox_bytes(capacity_tokens); }
+int amusd_mailbox_capacity(const amusd_session_desc* d) { return d ? mailbox_cap(d) : 0; }
+
+size_t amusd_session_bytes(const amusd_session_desc* d) {
+  if (!d) return 0;
+  return session_carve(d, session_max_seq(d), std::max(d->prompt_len, 1), nullptr, nullptr);
+}
+
+int amusd_session_create(amusd_session** out, amusd_model* draft, amusd_model* verify, const amusd_session_desc* d,
+                         void* mem, size_t mem_bytes, void* mb_local, void* mb_peer) {
+  if (!out || !d || !mem || !mb_local) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  if (!draft && !verify) return fail(AMUSD_ERR_INVALID_INPUT, "session needs a draft or a verify model");
+  if (d->prompt_len < 1) return fail(AMUSD_ERR_INVALID_INPUT, "prompt_length must be >= 1");
+  if (d->max_new_tokens < 1) return fail(AMUSD_ERR_INVALID_INPUT, "max_new_tokens must be >= 1");
+  if (d->draft_window_k < 1 || d->draft_window_k > KMAX - 1)
+    return fail(AMUSD_ERR_INVALID_INPUT, "draft_window_k must be in [1, 15]");
+  if (d->max_draft_lead < 0) return fail(AMUSD_ERR_INVALID_INPUT, "max_draft_lead must be >= 1 when set");
+  if (d->max_window < 1 || d->max_window > KMAX) return fail(AMUSD_ERR_INVALID_INPUT, "max_window must be in [1, 16]");
+  if (d->rho < 0.0 || d->rho > 1.0) return fail(AMUSD_ERR_INVALID_INPUT, "rho must be in [0, 1]");
+  if (d->trace_cap < 1) return fail(AMUSD_ERR_INVALID_INPUT, "trace_cap must be >= 1");
+  if (mem_bytes < amusd_session_bytes(d)) return fail(AMUSD_ERR_INVALID_INPUT, "session buffer too small");
+  const int need = d->prompt_len + d->max_new_tokens + KMAX + 2;
+  if (verify && verify->max_seq < need) return fail(AMUSD_ERR_INVALID_INPUT, "verify max_seq too small for prompt + max_new_tokens");
+  if (draft && draft->max_seq < need) return fail(AMUSD_ERR_INVALID_INPUT, "draft max_seq too small for prompt + max_new_tokens");
+  amusd_session* s = new amusd_session();
+  s->draft = draft;
+  s->verify = verify;
+  s->d = *d;
+  s->cap = mailbox_cap(d);
+  s->mb_local = (MailboxHdr*)mb_local;
+  s->mb_peer = mb_peer ? (MailboxHdr*)mb_peer : (MailboxHdr*)mb_local;
+  session_carve(d, session_max_seq(d), std::max(d->prompt_len, 1), mem, s);
+  s->coin.mode = draft ? d->coin_mode : AMUSD_COIN_NONE;
+  s->coin.always = d->rho >= 1.0;  // int(1.0 * 2**64) == 2**64 > every hash
+  s->coin.thr = s->coin.always ? ~0ull : (unsigned long long)(d->rho * 18446744073709551616.0);
+  if (draft) { s->coin.vocab = draft->vocab; s->coin.eos = draft->eos; s->coin.exclude_eos = draft->exclude_eos; }
+  s->coin.canon = d->canon;
+  s->coin.canon_len = d->canon ? d->canon_len : 0;
+  if (s->coin.mode == AMUSD_COIN_NONE) { s->coin.hash = nullptr; s->coin.onpath = nullptr; }
+  const char* nopdl = getenv("AMUSD_NO_PDL");
+  s->use_pdl = !(nopdl && nopdl[0] == '1');
+  if (cudaStreamCreateWithFlags(&s->capture, cudaStreamNonBlocking) != cudaSuccess) {
+    delete s;
+    return fail(AMUSD_ERR_CUDA, "stream create failed");
+  }
+  *out = s;
+  return AMUSD_OK;
+}
+
+int amusd_session_destroy(amusd_session* s) {
+  if (!s) return AMUSD_OK;
+  for (auto& e : s->exec)
+    for (auto& x : e)
+      if (x) cudaGraphExecDestroy(x);
+  if (s->capture) cudaStreamDestroy(s->capture);
+  delete s;
+  return AMUSD_OK;
+}
+
+int amusd_session_reset(amusd_session* s, const int32_t* prompt, int n, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!s || !prompt) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  if (n != s->d.prompt_len) return fail(AMUSD_ERR_INVALID_INPUT, "prompt length differs from the session's");
+  for (amusd_model* m : {s->draft, s->verify}) {
+    if (!m) continue;
+    if (int r = sync_from_device(m, st)) return r;
+    if (m->len != n || m->prompt_len != n)
+      return fail(AMUSD_ERR_INVALID_INPUT, "models must hold init_state(prompt) before a run");
+    if (m->kv_len > m->len - 1) m->kv_len = m->len - 1;
+    if (int r = push_header(m, st)) return r;
+  }
+  CUDA_TRY(cudaMemcpyAsync(s->prompt_dev, prompt, sizeof(int) * n, cudaMemcpyHostToDevice, st));
+  ProtoArgs a = make_args(s);
+  CUDA_TRY(launch_session_reset(a, s->prompt_dev, s->d.coin_seed, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return AMUSD_OK;
+}
+
+}  // extern "C"
+
+// Capture the body of one actor's loop into `body`.
+static int capture_body(amusd_session* s, int engine, int actor, cudaGraph_t body, cudaGraphConditionalHandle h) {
+  ProtoArgs a = make_args(s);
+  a.cond = h;
+  a.has_cond = 1;
+  cudaStream_t st = s->capture;
+  CUDA_TRY(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  int r = AMUSD_OK;
+  const bool pdl = s->use_pdl;
+  auto fwd = [&](amusd_model* m, StepCtl* c, int nr) { if (!r) r = model_forward(m, c, nr, st, pdl, false); };
+  auto pk = [&](int which, int arg) { if (!r && proto_launch(which, a, st, arg) != cudaSuccess) r = fail(AMUSD_ERR_CUDA, "protocol launch failed"); };
+  if (engine == AMUSD_ENGINE_AUTOREGRESSIVE) {
+    pk(kArBegin, 0); fwd(s->verify, s->vctl, KMAX); pk(kArEnd, 0);
+  } else if (engine == AMUSD_ENGINE_SYNC) {
+    pk(kSyncRoundBegin, 0);
+    for (int i = 0; i < s->d.draft_window_k; ++i) {
+      pk(kSyncDraftBegin, i); fwd(s->draft, s->dctl, 2); pk(kSyncDraftEnd, 0);
+    }
+    pk(kSyncVerifyBegin, 0); fwd(s->verify, s->vctl, KMAX); pk(kSyncVerifyEnd, 0);
+  } else if (actor == 0) {
+    pk(kDraftBegin, 0); fwd(s->draft, s->dctl, 2); pk(kDraftEnd, 0);
+  } else {
+    pk(kVerifyBegin, 0); fwd(s->verify, s->vctl, KMAX); pk(kVerifyEnd, 0);
+  }
+  cudaGraph_t g2 = body;
+  cudaError_t e = cudaStreamEndCapture(st, &g2);
+  if (r) return r;
+  CUDA_TRY(e);
+  return AMUSD_OK;
+}
+
+static int build_loop(amusd_session* s, int engine, int actor, cudaGraphExec_t* out) {
+  cudaGraph_t g;
+  CUDA_TRY(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  CUDA_TRY(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  CUDA_TRY(cudaGraphAddNode(&node, g, nullptr, 0, &p));
+  if (int r = capture_body(s, engine, actor, p.conditional.phGraph_out[0], h)) {
+    cudaGraphDestroy(g);
+    return r;
+  }
+  cudaError_t e = cudaGraphInstantiate(out, g, 0);
+  cudaGraphDestroy(g);
+  CUDA_TRY(e);
+  return AMUSD_OK;
+}
+
+extern "C" {
+
+int amusd_session_launch(amusd_session* s, int engine, void* verify_stream, void* draft_stream) {
+  if (!s) return fail(AMUSD_ERR_INVALID_INPUT, "null session");
+  if (engine < 0 || engine > AMUSD_ENGINE_ASYNC_VERIFY) return fail(AMUSD_ERR_INVALID_INPUT, "unknown engine");
+  const bool need_d = engine != AMUSD_ENGINE_AUTOREGRESSIVE && engine != AMUSD_ENGINE_ASYNC_VERIFY;
+  const bool need_v = engine != AMUSD_ENGINE_ASYNC_DRAFT;
+  if (need_d && !s->draft) return fail(AMUSD_ERR_INVALID_INPUT, "engine needs a draft model");
+  if (need_v && !s->verify) return fail(AMUSD_ERR_INVALID_INPUT, "engine needs a verify model");
+  if (engine == AMUSD_ENGINE_SYNC && s->d.draft_window_k + 1 > KMAX)
+    return fail(AMUSD_ERR_INVALID_INPUT, "draft_window_k too large");
+  const int actors[2] = {need_d && engine != AMUSD_ENGINE_AUTOREGRESSIVE && engine != AMUSD_ENGINE_SYNC,
+                         need_v || engine == AMUSD_ENGINE_SYNC};
+  for (int actor = 0; actor < 2; ++actor) {
+    if (!actors[actor]) continue;
+    if (!s->exec[engine][actor])
+      if (int r = build_loop(s, engine, actor, &s->exec[engine][actor])) return r;
+  }
+  if (s->draft) s->draft->dirty = true;
+  if (s->verify) s->verify->dirty = true;
+  if (actors[1]) CUDA_TRY(cudaGraphLaunch(s->exec[engine][1], (cudaStream_t)verify_stream));
+  if (actors[0]) CUDA_TRY(cudaGraphLaunch(s->exec[engine][0], (cudaStream_t)(draft_stream ? draft_stream : verify_stream)));
+  return AMUSD_OK;
+}
+
+int amusd_session_info(amusd_session* s, amusd_run_info* info, int32_t* V, int v_cap, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!s || !info) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  MailboxHdr h;
+  int counts[2];
+  CUDA_TRY(cudaMemcpyAsync(&h, s->mb_local, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(counts, s->dtrace.count, sizeof(counts), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  info->p_v = h.vb.p_v;
+  info->p_d = h.db.p_d;
+  info->complete = h.vb.complete;
+  info->error = h.vb.error ? h.vb.error : h.db.error;
+  info->verify_steps = h.vb.verify_steps;
+  info->rollbacks = h.vb.rollbacks;
+  info->drafted = h.db.drafted;
+  info->acks = h.db.acks;
+  info->n_draft_events = counts[0];
+  info->n_verify_events = counts[1];
+  if (V && v_cap > 0) {
+    const int nv = std::min(v_cap, std::max(0, h.vb.p_v - s->d.prompt_len));
+    if (nv) CUDA_TRY(cudaMemcpyAsync(V, mb_V(s->mb_local, s->cap), sizeof(int) * nv, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  return AMUSD_OK;
+}
+
+int amusd_session_trace(amusd_session* s, int actor, amusd_trace_event* out, int cap, int* n, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!s || !out || !n) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  const TraceDev& t = actor == 0 ? s->dtrace : s->vtrace;
+  int cnt = 0;
+  CUDA_TRY(cudaMemcpyAsync(&cnt, t.count, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  *n = cnt;
+  const int k = std::min(std::min(cnt, cap), t.cap);
+  if (k) CUDA_TRY(cudaMemcpyAsync(out, t.ev, sizeof(amusd_trace_event) * k, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return AMUSD_OK;
+}
+
+int amusd_session_kernels_per_step(amusd_session* s, int engine, int* draft_step, int* verify_step) {
+  if (!s || !draft_step || !verify_step) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  *draft_step = s->draft ? model_kernels_per_forward(s->draft) + 2 : 0;
+  *verify_step = s->verify ? model_kernels_per_forward(s->verify) + 2 : 0;
+  if (engine == AMUSD_ENGINE_SYNC) *verify_step += 1;
+  return AMUSD_OK;
+}
+
+}  // extern "C"
+
+// -------------------------------------------------------- weight fill
+__global__ void k_fill_uniform(void* dst, int dtype, size_t n, unsigned long long seed, float scale) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const unsigned long long z = mix64(seed + i);
+    const float u = (float)(z >> 40) * (1.0f / 16777216.0f);  // [0, 1)
+    const float v = scale * (2.0f * u - 1.0f);
+    if (dtype == AMUSD_BF16) ((__nv_bfloat16*)dst)[i] = __float2bfloat16(v);
+    else ((float*)dst)[i] = v;
+  }
+}
+
+extern "C" int amusd_fill_uniform(void* dst, int dtype, size_t n, uint64_t seed, float scale, void* stream) {
+  if (!dst) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  k_fill_uniform<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(dst, dtype, n, seed, scale);
+  CUDA_TRY(cudaGetLastError());
+  return AMUSD_OK;
+}
