@@ -26,7 +26,7 @@ from . import _lib as L
 from .coordination import SharedDecodeState
 from .errors import InvalidInputError, ProtocolViolationError, SpecDecError
 from .metrics import DecodeStats, DecodeTrace, summarize, trace_from_device
-from .models import AgreementDraft, CudaModel, ModelState
+from .models import AgreementDraft, CudaModel, ModelState, settle
 
 FINISHED_BY_EOS = "eos"
 FINISHED_BY_LENGTH = "length_limit"
@@ -135,7 +135,7 @@ class DeviceSession:
             raise InvalidInputError("AgreementDraft needs the canonical verify path (canon)")
         self.canon = canon
         n = config.max_new_tokens
-        cap = trace_cap or (4 * (n + 64) + 256)
+        cap = trace_cap or ((config.draft_window_k + 2) * (n + 2 * L.KMAX) + 16 * (n + 64) + 1024)
         self.desc = L.SessionDesc(
             prompt_len=prompt_len, max_new_tokens=n, draft_window_k=config.draft_window_k,
             max_draft_lead=config.max_draft_lead or 0, max_window=max_window, coin_mode=coin_mode,
@@ -153,6 +153,7 @@ class DeviceSession:
             C.byref(self._h), dm.handle if dm else None, vm.handle if vm else None, C.byref(self.desc),
             C.c_void_p(self.mem.data_ptr()), sbytes, C.c_void_p(self.mailbox.data_ptr()),
             C.c_void_p(mb_peer) if mb_peer else None))
+        settle(self.device)
         self._trace_buf = (L.TraceEvent * cap)()
         self._v_buf = (C.c_int32 * (self.mb_cap + 1))()
 
@@ -204,7 +205,9 @@ class DeviceSession:
                 cnt = C.c_int()
                 L.check(self.lib.amusd_session_trace(self._h, actor, self._trace_buf, len(self._trace_buf),
                                                      C.byref(cnt), vs.cuda_stream))
-                k = min(cnt.value, len(self._trace_buf))
+                if cnt.value > len(self._trace_buf):
+                    raise SpecDecError(f"trace ring overflow ({cnt.value} events > {len(self._trace_buf)})")
+                k = cnt.value
                 rows.append([(e.t_ns, e.busy_ns, e.kind, e.pos_lo, e.pos_hi, e.draft_accepted)
                              for e in self._trace_buf[:k]])
         if info.error:
@@ -263,6 +266,7 @@ def canonical_path(verify, prompt: Sequence[int], n: int) -> torch.Tensor:
         out = _session(None, verify, len(prompt), cfg).run(L.ENGINE_AR, prompt)
         toks = list(prompt) + out.verified
         _CANON[key] = torch.tensor(toks, dtype=torch.int32, device=vm.device)
+        settle(vm.device)
     return _CANON[key]
 
 

@@ -136,8 +136,9 @@ def trace_from_device(draft_rows, verify_rows, prompt_length: int, final_pos: in
             ev = TraceEvent((t_ns - t0) / 1e6, actor, _DEVICE_KINDS[kind], int(lo), int(hi), busy_ns / 1e6, int(acc))
             logs[actor].append((ev.t_ms, seq, ev))
             seq += 1
-    for lg in logs.values():
-        lg.sort(key=lambda x: (x[0], x[1]))
+    # Each ring is already in true program order (single writer, sequential
+    # kernels); %globaltimer can differ by a few hundred ns between SMs, so
+    # rings are never re-sorted -- only merged, then clamped.
     events = merge_actor_logs(logs[ACTOR_DRAFT], logs[ACTOR_VERIFY])
     t_end = max((t_done - t0) / 1e6, events[-1].t_ms if events else 0.0)
     events.append(TraceEvent(t_end, ACTOR_VERIFY, COMPLETE, final_pos, final_pos))

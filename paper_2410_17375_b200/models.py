@@ -44,6 +44,15 @@ def device_stream(device=None) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+def settle(device) -> None:
+    """Wait for allocation/initialisation work torch queued on its current stream.
+
+    Device buffers are created with torch (zero fills, weight init) on the
+    current stream, but the decode loops run on their own non-blocking
+    streams; without this a late fill could land on live state."""
+    torch.cuda.current_stream(device).synchronize()
+
+
 @dataclass
 class ModelState:
     """Handle on a model's device-resident sequence (models.py:58-82)."""
@@ -173,6 +182,7 @@ class HashChainModel(CudaModel):
         self._state = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
         L.check(self._lib.amusd_hash_create(C.byref(self._h), self.seed, vocab_size, eos_token, int(exclude_eos),
                                             float(_rho), max_seq, C.c_void_p(self._state.data_ptr()), nbytes))
+        settle(self.device)
 
     def kernels_per_forward(self) -> int:
         return 1
@@ -341,6 +351,7 @@ class TransformerModel(CudaModel):
         self._state = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
         L.check(self._lib.amusd_tf_create(C.byref(self._h), C.byref(cfg), C.byref(w),
                                           C.c_void_p(self._state.data_ptr()), nbytes))
+        settle(self.device)
 
     def _synthetic(self, tdt, seed: int, std: float) -> dict:
         """Deterministic random init on the GPU: uniform with the given std, norms = 1."""
