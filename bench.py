@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""AMUSD decode benchmark (BASELINE.json metric): generated tokens/s, greedy,
+bs=1, AMUSD vs sync-SD vs AR, with the HBM roofline of the dominant kernel.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl amusd|reference]
+
+N=1 workload = BASELINE configs[2] (configs[1]'s pair co-located on one
+B200): Llama-3.2-1B-shaped draft + Llama-3.1-8B-shaped verify, random-init
+bf16, synthetic 32-token prompt, 512 new tokens, agreement coin rho=0.8.
+A "step" is one full decode of 512 tokens.  N>1 (torchrun, one process per
+GPU): every rank runs an independent co-located pair ("replicas"; weak
+scaling, no data-path collective), value = all tokens / max-over-ranks time.
+
+--impl reference times the CPU restatement of the reference path (oracle/,
+numpy fp32, two-thread AMUSD executor) on the host cores, bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import random
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "generated tokens/sec (greedy, bs=1) AMUSD vs sync-SD vs AR; % HBM roofline"
+WORKLOAD = ("cfg3: Llama-3.2-1B-shaped draft + Llama-3.1-8B-shaped verify co-located on 1xB200 "
+            "(draft/verify on separate CUDA streams), random-init bf16, 32-token prompt, 512 new tokens")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="amusd", choices=["amusd", "reference"])
+    ap.add_argument("--new-tokens", type=int, default=512)
+    ap.add_argument("--prompt-len", type=int, default=32)
+    ap.add_argument("--rho", type=float, default=0.8)
+    ap.add_argument("--k", type=int, default=4)
+    ap.add_argument("--lead", type=int, default=0, help="max_draft_lead (0 = None)")
+    ap.add_argument("--window", type=int, default=16)
+    ap.add_argument("--shapes", default="1b8b", choices=["1b8b", "tiny"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-tokens", type=int, default=4)
+    ap.add_argument("--profile-only", action="store_true", help="one AMUSD decode, no extras (for ncu)")
+    return ap.parse_args()
+
+
+def synthetic_prompt(n: int, vocab: int) -> list:
+    rng = random.Random(1234)
+    return [rng.randrange(3, vocab) for _ in range(n)]
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.proc, self.path = gpu, None, None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 7 and parts[0].replace(".", "").isdigit():
+                    rows.append(parts)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in rows]
+        loaded = [float(r[0]) for r in rows if float(r[2]) > 250.0] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[3:7]) if v.lower().startswith("active")})
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(float(r[1]) for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------- GPU arm
+def gpu_arm(args, rank: int, world: int, local_rank: int):
+    import torch
+    import paper_2410_17375_b200 as P
+    from paper_2410_17375_b200 import _lib as L
+    from paper_2410_17375_b200.engines import DeviceSession, canonical_path, finalize_tokens
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    TC = P.TransformerConfig
+    N, Plen = args.new_tokens, args.prompt_len
+    max_seq = Plen + N + 2 * L.KMAX + 32
+    if args.shapes == "tiny":
+        vcfg, dcfg = TC.tiny_verify(max_seq=max_seq), TC.tiny_draft(max_seq=max_seq)
+    else:
+        vcfg, dcfg = TC.llama_8b(max_seq=max_seq), TC.llama_1b(max_seq=max_seq)
+    vm = P.TransformerModel(vcfg, seed=0, device=dev)
+    dm = P.TransformerModel(dcfg, seed=1, device=dev)
+    prompt = synthetic_prompt(Plen, vcfg.vocab_size)
+    draft = P.AgreementDraft(dm, args.rho, coin_seed=1234)
+    cfg = P.DecodeConfig(max_new_tokens=N, draft_window_k=args.k, max_draft_lead=args.lead or None)
+    if args.profile_only:  # natural draft, no canonical AR pass: keeps the ncu launch list short
+        s = DeviceSession(dm, vm, Plen, cfg, max_window=args.window)
+        out = s.run(L.ENGINE_ASYNC, prompt)
+        torch.cuda.synchronize()
+        print(json.dumps({"profile_only": True, "verified": len(out.verified), "verify_steps": out.info.verify_steps,
+                          "draft_iters": out.info.draft_iters}))
+        return None
+    canon = canonical_path(vm, prompt, N + L.KMAX)  # setup: the verify model's greedy path (coin input)
+    sess = {
+        "ar": (DeviceSession(None, vm, Plen, cfg), L.ENGINE_AR),
+        "sync": (DeviceSession(draft, vm, Plen, cfg, canon=canon), L.ENGINE_SYNC),
+        "amusd": (DeviceSession(draft, vm, Plen, cfg, canon=canon, max_window=args.window), L.ENGINE_ASYNC),
+    }
+    kd, kv = sess["amusd"][0].kernels_per_step(L.ENGINE_ASYNC)
+    _, kv_sync = sess["sync"][0].kernels_per_step(L.ENGINE_SYNC)
+    results, ref_tokens = {}, None
+    sampler = None
+    for name in ("ar", "sync", "amusd"):
+        s, eng = sess[name]
+        for _ in range(args.warmup):
+            s.run(eng, prompt)
+        per, toks, launches, stats = [], 0, 0, []
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        cm = ClockSampler(local_rank) if name == "amusd" else None
+        if cm:
+            cm.__enter__()
+        for _ in range(args.steps):
+            s.prepare(prompt)                      # prefill is reported separately (not timed)
+            start, end = s.launch(eng)
+            out = s.collect(start, end)
+            tokens, _ = finalize_tokens(out.verified, vm.eos_token, N)
+            per.append(out.device_ms)
+            toks += len(tokens)
+            if name == "ar":
+                launches += out.info.verify_iters * (kv - 2 + 2)
+            elif name == "sync":
+                launches += out.info.verify_iters * (args.k * kd + kv_sync)
+            else:
+                launches += out.info.draft_iters * kd + out.info.verify_iters * kv
+            stats.append(out.info)
+            if ref_tokens is None:
+                ref_tokens = tokens
+            elif tokens != ref_tokens:
+                raise SystemExit(f"{name} output differs from the AR oracle -- parity broken")
+        torch.cuda.synchronize()
+        if cm:
+            cm.__exit__(None, None, None)
+            sampler = cm
+        total_ms = sum(per)
+        if world > 1:
+            t = torch.tensor([total_ms], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            total_ms = float(t.item())
+        results[name] = {
+            "tokens_per_s": toks / (total_ms / 1000.0), "ms_per_step": total_ms / args.steps,
+            "ms_per_token": total_ms / toks, "generated": toks // args.steps, "gpu_launches": launches,
+            "verify_steps": statistics.mean(i.verify_steps for i in stats),
+            "rollbacks": statistics.mean(i.rollbacks for i in stats),
+            "drafted": statistics.mean(i.drafted for i in stats),
+        }
+    # ---- kernel roofline: time the forwards / dominant kernel in isolation (CUDA events)
+    import ctypes as C
+    lib = L.load()
+
+    def time_fwd(m, rows, which, layer=0, iters=20):
+        ms = C.c_float()
+        L.check(lib.amusd_time_forward(m.handle, rows, which, layer, iters, C.byref(ms),
+                                       torch.cuda.current_stream().cuda_stream))
+        return ms.value
+    vm.init_state(prompt)
+    dm.init_state(prompt)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if peaks else "fallback"
+    gu_bytes = 2 * vcfg.ffn * vcfg.d_model * vcfg.elem_bytes
+    gu_ms = time_fwd(vm, 4, 3, layer=vcfg.n_layers // 2, iters=50)  # tcgen05 gate/up (16-row path)
+    v_ms = time_fwd(vm, 1, -1, iters=5)
+    v4_ms = time_fwd(vm, 4, -1, iters=5)
+    d_ms = time_fwd(dm, 1, -1, iters=10)
+    kernels = {
+        "verify_gate_up_gemv": {"bytes": gu_bytes, "ms": gu_ms, "gbs": gu_bytes / gu_ms / 1e6},
+        "verify_forward_m1": {"bytes": vcfg.step_weight_bytes(), "ms": v_ms, "gbs": vcfg.step_weight_bytes() / v_ms / 1e6},
+        "verify_forward_m4": {"bytes": vcfg.step_weight_bytes(), "ms": v4_ms, "gbs": vcfg.step_weight_bytes() / v4_ms / 1e6},
+        "draft_forward_m1": {"bytes": dcfg.step_weight_bytes(), "ms": d_ms, "gbs": dcfg.step_weight_bytes() / d_ms / 1e6},
+    }
+    traffic = None
+    prof = ROOT / "profiles" / "dominant_kernel_traffic.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "kernel": "verify gate/up GEMV (8B, m<=16 rows, RMSNorm+SiLU fused)",
+                "achieved": round(kernels["verify_gate_up_gemv"]["gbs"], 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(kernels["verify_gate_up_gemv"]["gbs"] / hbm_peak, 4), "traffic": traffic,
+                "algorithmic_bytes_per_launch": gu_bytes, "peak_source": peak_src,
+                "forwards": {k: {"ms": round(v["ms"], 4), "GB/s": round(v["gbs"], 1),
+                                 "frac": round(v["gbs"] / hbm_peak, 4)} for k, v in kernels.items()}}
+    # ---- end to end through the public API (host prompt in, host tokens out, wall clock)
+    e2e = None
+    if rank == 0 or world > 1:
+        e2e_ms, e2e_toks = [], 0
+        for i in range(max(1, args.steps)):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = P.decode_speculative_async(draft, vm, prompt, cfg,
+                                             executor=P.CudaAsyncExecutor(max_window=args.window))
+            torch.cuda.synchronize()
+            e2e_ms.append((time.perf_counter() - t0) * 1000.0)
+            e2e_toks += len(res.tokens)
+            if res.tokens != ref_tokens:
+                raise SystemExit("e2e output differs from the AR oracle")
+        h2d = 4 * Plen * 3 + 256 * (2 + (Plen + L.KMAX - 1) // L.KMAX * 2)   # prompt copies + prefill control blocks
+        d2h = 4 * (N + L.KMAX) + 256 + 32 * (results["amusd"]["drafted"] + results["amusd"]["verify_steps"] + 64)
+        e2e = {"value": round(e2e_toks / (sum(e2e_ms) / 1000.0), 2), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "includes": "prefill of both models + graph launch + V/trace read-back + trace merge"}
+    return {"results": results, "roofline": roofline, "e2e": e2e, "clocks": sampler.summary() if sampler else None,
+            "vm": vm, "dm": dm, "prompt": prompt, "canon": canon.tolist(), "vcfg": vcfg, "dcfg": dcfg}
+
+
+# --------------------------------------------------------------- CPU arm
+def cpu_models(vm, dm, vcfg, dcfg):
+    from oracle.ref_decoder import RefDecoder, TfShape
+
+    def mk(m, c):
+        shp = TfShape(c.vocab_size, c.d_model, c.n_layers, c.n_heads, c.n_kv_heads, c.head_dim, c.ffn,
+                      eos=c.eos_token, exclude_eos=c.exclude_eos, eps=c.norm_eps, theta=c.rope_theta, kv_bf16=True)
+        return RefDecoder(shp, m.host_weights(), tied=c.tied)
+    return mk(vm, vcfg), mk(dm, dcfg)
+
+
+def cpu_sample(rv, rd, prompt, canon, rho, n_tokens: int) -> dict:
+    """Bounded CPU sample: reference AR and two-thread AMUSD on the numpy models."""
+    from oracle import specdec_oracle as O
+    from oracle.ref_decoder import CanonCoinDraft
+    cd = CanonCoinDraft(rd, canon, rho, 1234)
+    t0 = time.perf_counter()
+    O.decode_ar(rv, prompt, n_tokens)
+    ar_s = time.perf_counter() - t0
+    toks, _, cnt, wall = O.thread_async(cd, rv, prompt, n_tokens)
+    return {"amusd_tokens_per_s": len(toks) / wall, "ar_tokens_per_s": n_tokens / ar_s, "amusd_wall_s": wall,
+            "ar_wall_s": ar_s}
+
+
+def reference_arm(args, rank: int, world: int):
+    """--impl reference: the CPU restatement of the path timed on the host cores."""
+    import numpy as np  # noqa: F401
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    try:
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("weights are generated on the GPU (synthetic bf16 init) then copied to the host")
+        import paper_2410_17375_b200 as P
+        from paper_2410_17375_b200 import _lib as L
+        from paper_2410_17375_b200.engines import canonical_path
+        TC = P.TransformerConfig
+        N, Plen = args.new_tokens, args.prompt_len
+        max_seq = Plen + N + 2 * L.KMAX + 32
+        if args.shapes == "tiny":
+            vcfg, dcfg = TC.tiny_verify(max_seq=max_seq), TC.tiny_draft(max_seq=max_seq)
+        else:
+            vcfg, dcfg = TC.llama_8b(max_seq=max_seq), TC.llama_1b(max_seq=max_seq)
+        vm = P.TransformerModel(vcfg, seed=0)
+        dm = P.TransformerModel(dcfg, seed=1)
+        prompt = synthetic_prompt(Plen, vcfg.vocab_size)
+        canon = canonical_path(vm, prompt, N + L.KMAX).tolist()
+        rv, rd = cpu_models(vm, dm, vcfg, dcfg)
+        del vm, dm
+        torch.cuda.empty_cache()
+    except Exception as exc:  # pragma: no cover - only on a box without the GPU stack
+        print(json.dumps({"impl": "reference", "unavailable": f"{type(exc).__name__}: {exc}"}))
+        return
+    from oracle import specdec_oracle as O
+    from oracle.ref_decoder import CanonCoinDraft
+    cd = CanonCoinDraft(rd, canon, args.rho, 1234)
+    sample = max(1, args.cpu_tokens // 2)
+    for _ in range(args.warmup):
+        O.thread_async(cd, rv, prompt, 1)
+    walls, toks = [], 0
+    for _ in range(args.steps):
+        t, _, _, wall = O.thread_async(cd, rv, prompt, sample)
+        walls.append(wall)
+        toks += len(t)
+    v = toks / sum(walls)
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1000 * sum(walls) / args.steps, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (random-init weights, seeded prompt)",
+            "config": {"workload": WORKLOAD, "rho": args.rho, "new_tokens_per_step": sample},
+            "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "cores": cores, "kind": "port",
+                             "sample": f"AMUSD two-thread executor (oracle restatement of engines.py:409-531) on "
+                                       f"numpy fp32 1B/8B-shaped decoders, {sample} new tokens per step"},
+            "e2e": {"value": round(v, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# -------------------------------------------------------------------- main
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world > 1:
+        import torch
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl" if args.impl == "amusd" else "gloo")
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+    else:
+        out = gpu_arm(args, rank, world, local_rank)
+        if out is None:
+            return
+        res = out["results"]
+        cpu = None
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            rv, rd = cpu_models(out["vm"], out["dm"], out["vcfg"], out["dcfg"])
+            s = cpu_sample(rv, rd, out["prompt"], out["canon"], args.rho, args.cpu_tokens)
+            cpu = {"value": round(s["amusd_tokens_per_s"], 4), "unit": "tokens/s", "cores": os.cpu_count(),
+                   "kind": "port",
+                   "sample": f"{args.cpu_tokens} new tokens, AMUSD two-thread executor + AR on numpy fp32 "
+                             f"1B/8B-shaped decoders (oracle/), same prompt/weights/rho",
+                   "ar_tokens_per_s": round(s["ar_tokens_per_s"], 4)}
+        if rank == 0:
+            a, sy, ar = res["amusd"], res["sync"], res["ar"]
+            line = {
+                "metric": METRIC, "value": round(a["tokens_per_s"] * world, 2), "unit": "tokens/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(a["ms_per_step"], 3),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (random-init weights, seeded 32-token prompt)",
+                "config": {"workload": WORKLOAD if args.shapes == "1b8b" else "tiny pair (cfg1 shapes)",
+                           "rho": args.rho, "sync_k": args.k, "max_draft_lead": args.lead or None,
+                           "max_window": args.window, "new_tokens": args.new_tokens,
+                           "prompt_len": args.prompt_len, "parallelism": f"replicas x{world}" if world > 1 else "co-located pair",
+                           "l2": "weights (17.5 GB) >> 126 MB L2: no flush needed"},
+                "amusd": {k: round(v, 3) for k, v in a.items()},
+                "sync_sd": {k: round(v, 3) for k, v in sy.items()},
+                "ar": {k: round(v, 3) for k, v in ar.items()},
+                "speedup_vs_sync": round(a["tokens_per_s"] / sy["tokens_per_s"], 3),
+                "speedup_vs_ar": round(a["tokens_per_s"] / ar["tokens_per_s"], 3),
+                "roofline": out["roofline"], "cpu_baseline": cpu, "e2e": out["e2e"],
+                "gpu_launches": int(a["gpu_launches"]), "clocks": out["clocks"],
+            }
+            print(json.dumps(line))
+    if world > 1:
+        import torch
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

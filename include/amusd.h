@@ -159,6 +159,7 @@ typedef struct {
   int p_v, p_d, complete, error;
   int verify_steps, rollbacks, drafted, acks;
   int n_draft_events, n_verify_events;
+  int draft_iters, verify_iters;  /* loop-body executions (launch accounting) */
 } amusd_run_info;
 int amusd_session_info(amusd_session* s, amusd_run_info* info, int32_t* V, int v_cap, void* stream);
 
@@ -175,6 +176,12 @@ int amusd_session_trace(amusd_session* s, int actor /*0 draft, 1 verify*/, amusd
 /* ---------------------------------------------------------------- misc */
 int amusd_abi_version(void);
 const char* amusd_last_error(void);
+/* Benchmark helper: `iters` eager launches of one model forward over `rows`
+ * rows at the current cache position (state is not advanced), timed with
+ * CUDA events on `stream`; *ms = mean ms per launch.  which = -1 whole
+ * forward, else one kernel of layer `layer`: 0 QKV gemv, 1 attention, 2 O
+ * gemv, 3 gate/up gemv, 4 down gemv, 5 LM-head gemv, 6 argmax reduce. */
+int amusd_time_forward(amusd_model* m, int rows, int which, int layer, int iters, float* ms, void* stream);
 /* Number of kernels one step of `engine` launches (gpu_launches accounting). */
 int amusd_session_kernels_per_step(amusd_session* s, int engine, int* draft_step, int* verify_step);
 /* Device-side deterministic weight fill: w[i] = scale * u(splitmix64(seed + i)),

@@ -46,7 +46,8 @@ class SessionDesc(C.Structure):
 
 class RunInfo(C.Structure):
     _fields_ = [(n, C.c_int) for n in ("p_v", "p_d", "complete", "error", "verify_steps", "rollbacks",
-                                         "drafted", "acks", "n_draft_events", "n_verify_events")]
+                                         "drafted", "acks", "n_draft_events", "n_verify_events",
+                                         "draft_iters", "verify_iters")]
 
 
 class TraceEvent(C.Structure):
@@ -80,6 +81,7 @@ SIGNATURES = [
     ("amusd_session_launch", _I, [_VP, _I, _VP, _VP]),
     ("amusd_session_info", _I, [_VP, _P(RunInfo), _P(C.c_int32), _I, _VP]),
     ("amusd_session_trace", _I, [_VP, _I, _P(TraceEvent), _I, _P(_I), _VP]),
+    ("amusd_time_forward", _I, [_VP, _I, _I, _I, _I, _P(C.c_float), _VP]),
     ("amusd_session_kernels_per_step", _I, [_VP, _I, _P(_I), _P(_I)]),
     ("amusd_fill_uniform", _I, [_VP, _I, _SZ, C.c_uint64, C.c_float, _VP]),
 ]

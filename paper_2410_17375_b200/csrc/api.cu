@@ -18,6 +18,7 @@
 #include "internal.h"
 #include "protocol.h"
 #include "transformer.h"
+#include "gemm_tc.h"
 
 using namespace amusd;
 
@@ -78,11 +79,32 @@ struct amusd_model {
   amusd_tf_weights w{};
   void *kc = nullptr, *vc = nullptr;
   float *h = nullptr, *qkv = nullptr, *attn = nullptr, *act = nullptr, *logits = nullptr;
+  float* attn_ws = nullptr;
+  int* attn_cnt = nullptr;
   unsigned long long* part = nullptr;
   int lm_grid = 0;
   size_t kv_layer_elems = 0;
   int last_rows = 0;
+  // tensor-core (tcgen05) path for 16-row forwards
+  bool tc = false;
+  __nv_bfloat16 *xa_b = nullptr, *attn_b = nullptr, *act_b = nullptr;
+  float* inv = nullptr;
+  float* ssp = nullptr;
+  float* tc_ws = nullptr;
+  int* tc_cnt = nullptr;
+  // weights re-laid-out as tile-contiguous SW128 16 KB units (one bulk copy each)
+  std::vector<const uint8_t*> wt_qkv, wt_o, wt_gu, wt_d;
+  const uint8_t* wt_lm = nullptr;
+  uint8_t* tiled = nullptr;
+  CUtensorMap map_xa{}, map_attn{}, map_act{};
 };
+
+static bool tc_shapes_ok(const amusd_tf_config* c) {
+  const int ncols = (c->n_heads + 2 * c->n_kv_heads) * c->head_dim;
+  // tcgen05 tiles: 128 weight rows (64 gate + 64 up features) x 64 K per unit
+  return c->dtype == AMUSD_BF16 && c->use_tensor_cores && c->d_model % 128 == 0 && ncols % 128 == 0 &&
+         c->ffn % 64 == 0 && c->vocab % 128 == 0 && (c->n_heads * c->head_dim) % 64 == 0;
+}
 
 static size_t tf_carve(const amusd_tf_config* c, void* base, amusd_model* m) {
   Carver cv(base);
@@ -99,9 +121,33 @@ static size_t tf_carve(const amusd_tf_config* c, void* base, amusd_model* m) {
   float* qkv = cv.take<float>((size_t)KMAX * ncols);
   float* attn = cv.take<float>((size_t)KMAX * c->n_heads * c->head_dim);
   float* act = cv.take<float>((size_t)KMAX * c->ffn);
-  unsigned long long* part = cv.take<unsigned long long>((size_t)KMAX * lm_grid);
+  const int lm_tiles = (c->vocab + 127) / 128;
+  unsigned long long* part = cv.take<unsigned long long>((size_t)KMAX * std::max(lm_grid, lm_tiles));
   float* logits = cv.take<float>((size_t)KMAX * c->vocab);
+  const int group = c->n_heads / std::max(1, c->n_kv_heads);
+  float* attn_ws = cv.take<float>((size_t)c->n_kv_heads * KMAX * attn_max_splits(c->max_seq) * group * (c->head_dim + 2));
+  int* attn_cnt = cv.take<int>((size_t)c->n_kv_heads * KMAX);
+  const bool tc = tc_shapes_ok(c);
+  __nv_bfloat16 *xa_b = nullptr, *attn_b = nullptr, *act_b = nullptr;
+  float *inv = nullptr, *ws = nullptr, *ssp_b = nullptr;
+  int* cnt = nullptr;
+  uint8_t* tiled = nullptr;
+  if (tc) {
+    xa_b = cv.take<__nv_bfloat16>((size_t)KMAX * c->d_model);
+    attn_b = cv.take<__nv_bfloat16>((size_t)KMAX * c->n_heads * c->head_dim);
+    act_b = cv.take<__nv_bfloat16>((size_t)KMAX * c->ffn);
+    inv = cv.take<float>(KMAX);
+    ssp_b = cv.take<float>((size_t)KMAX * (c->d_model / 128));
+    ws = cv.take<float>((size_t)256 * 2 * 128 * KMAX);  // >= grid (SM count) x 2 partial tiles of 128 x 16
+    cnt = cv.take<int>(std::max(lm_tiles, 4096));
+    const int hh = c->n_heads * c->head_dim;
+    const size_t per_layer = tc::tiled_bytes(ncols, c->d_model) + tc::tiled_bytes(c->d_model, hh) +
+                             tc::tiled_bytes(2 * c->ffn, c->d_model) + tc::tiled_bytes(c->d_model, c->ffn);
+    tiled = cv.take<uint8_t>(per_layer * c->n_layers + tc::tiled_bytes(c->vocab, c->d_model));
+  }
   if (m) {
+    m->attn_ws = attn_ws; m->attn_cnt = attn_cnt;
+    m->tc = tc; m->xa_b = xa_b; m->attn_b = attn_b; m->act_b = act_b; m->inv = inv; m->ssp = ssp_b; m->tc_ws = ws; m->tc_cnt = cnt; m->tiled = tiled;
     m->seq = seq; m->tok = tok; m->api_ctl = ctl; m->kc = kc; m->vc = vc; m->h = h; m->qkv = qkv;
     m->attn = attn; m->act = act; m->part = part; m->logits = logits; m->lm_grid = lm_grid;
     m->kv_layer_elems = (size_t)c->n_kv_heads * c->max_seq * c->head_dim;
@@ -119,57 +165,158 @@ static size_t hash_carve(int max_seq, void* base, amusd_model* m) {
   return align_up(cv.off, 256);
 }
 
+// One kernel of a transformer forward: which = 0 QKV gemv, 1 attention, 2 O
+// gemv, 3 gate/up gemv, 4 down gemv (per layer), 5 LM head, 6 argmax reduce,
+// 7 embedding.
+static int tf_kernel(amusd_model* m, StepCtl* ctl, int nr, int l, int which, cudaStream_t st, bool pdl,
+                     bool want_logits) {
+  const amusd_tf_config& c = m->cfg;
+  const int dt = c.dtype;
+  const size_t wsz = dt == AMUSD_BF16 ? 2 : 4;
+  const int d = c.d_model, hd = c.head_dim, H = c.n_heads, KV = c.n_kv_heads;
+  const int ncols = (H + 2 * KV) * hd;
+  GemvArgs g{};
+  g.ctl = ctl; g.eps = c.norm_eps; g.eos = c.eos_token; g.exclude_eos = c.exclude_eos;
+  switch (which) {
+    case 7:
+      CUDA_TRY(launch_embed(dt, ctl, m->w.embed, m->h, d, st, pdl));
+      break;
+    case 0:  // QKV (attention RMSNorm fused)
+      g.x = m->h; g.ldx = d; g.gamma = m->w.attn_norm[l]; g.W = m->w.wqkv[l]; g.N = ncols; g.K = d;
+      g.kc = gemv_kc(nr, d); g.out = m->qkv; g.ldo = ncols;
+      CUDA_TRY(launch_gemv(nr, dt, kEpiStore, g, st, pdl));
+      break;
+    case 1: {  // attention (RoPE + KV append fused)
+      AttnArgs at{};
+      at.ctl = ctl; at.qkv = m->qkv;
+      at.kc = (char*)m->kc + (size_t)l * m->kv_layer_elems * wsz;
+      at.vc = (char*)m->vc + (size_t)l * m->kv_layer_elems * wsz;
+      at.cos = m->w.rope_cos; at.sin = m->w.rope_sin; at.out = m->attn; at.ldo = H * hd;
+      at.H = H; at.KV = KV; at.hd = hd; at.S = c.max_seq; at.scale = 1.0f / sqrtf((float)hd);
+      at.ws = m->attn_ws; at.counters = m->attn_cnt; at.max_splits = attn_max_splits(c.max_seq);
+      CUDA_TRY(launch_attention(dt, at, st, pdl));
+      break;
+    }
+    case 2:  // O projection + residual
+      g.x = m->attn; g.ldx = H * hd; g.W = m->w.wo[l]; g.N = d; g.K = H * hd;
+      g.kc = gemv_kc(nr, H * hd); g.out = m->h; g.ldo = d;
+      CUDA_TRY(launch_gemv(nr, dt, kEpiResid, g, st, pdl));
+      break;
+    case 3:  // gate/up (MLP RMSNorm + SiLU*mul fused)
+      g.x = m->h; g.ldx = d; g.gamma = m->w.mlp_norm[l]; g.W = m->w.wgate[l]; g.W2 = m->w.wup[l];
+      g.N = c.ffn; g.K = d; g.kc = gemv_kc(nr, d); g.out = m->act; g.ldo = c.ffn;
+      CUDA_TRY(launch_gemv(nr, dt, kEpiGateUp, g, st, pdl));
+      break;
+    case 4:  // down projection + residual
+      g.x = m->act; g.ldx = c.ffn; g.W = m->w.wdown[l]; g.N = d; g.K = c.ffn; g.kc = gemv_kc(nr, c.ffn);
+      g.out = m->h; g.ldo = d;
+      CUDA_TRY(launch_gemv(nr, dt, kEpiResid, g, st, pdl));
+      break;
+    case 5:  // final RMSNorm + LM head + per-CTA argmax
+      g.x = m->h; g.ldx = d; g.gamma = m->w.final_norm; g.W = m->w.lm_head; g.N = c.vocab; g.K = d;
+      g.kc = gemv_kc(nr, d); g.part = m->part; g.logits = want_logits ? m->logits : nullptr;
+      CUDA_TRY(launch_gemv(nr, dt, kEpiArgmax, g, st, pdl));
+      break;
+    case 6:
+      CUDA_TRY(launch_argmax_final(ctl, m->part, m->lm_grid, st, pdl));
+      break;
+    default:
+      return fail(AMUSD_ERR_INVALID_INPUT, "unknown kernel id");
+  }
+  return AMUSD_OK;
+}
+
+// One kernel of the tensor-core forward (bf16, 16 rows): which = 0 QKV gemm,
+// 1 attention, 2 O gemm (+residual, emits mlp-norm input), 3 gate/up gemm,
+// 4 down gemm (+residual, emits next attn-norm input) per layer; 5 LM-head
+// gemm, 6 argmax reduce, 7 embedding (emits layer-0 attn-norm input).
+static int tc_kernel(amusd_model* m, StepCtl* ctl, int l, int which, cudaStream_t st, bool pdl,
+                     bool want_logits = false) {
+  const amusd_tf_config& c = m->cfg;
+  const int d = c.d_model, hd = c.head_dim, H = c.n_heads, KV = c.n_kv_heads;
+  const int ncols = (H + 2 * KV) * hd;
+  tc::TcArgs g{};
+  g.ctl = ctl; g.eos = c.eos_token; g.exclude_eos = c.exclude_eos; g.ws = m->tc_ws; g.counters = m->tc_cnt;
+  g.ssp_tiles = d / 128; g.norm_dim = (float)d; g.eps = c.norm_eps;
+  switch (which) {
+    case 7: CUDA_TRY(tc::launch_embed_tc(ctl, m->w.embed, m->h, m->w.attn_norm[0], m->xa_b, m->ssp, d, st, pdl)); break;
+    case 0:
+      g.epi = tc::kTcStoreScaled; g.ntiles = ncols / 128; g.kb = d / 64; g.N = ncols; g.ssp_in = m->ssp;
+      g.out = m->qkv; g.ldo = ncols;
+      g.wt = m->wt_qkv[l];
+      CUDA_TRY(tc::launch_gemm_tc(m->map_xa, g, st, pdl));
+      break;
+    case 1: {
+      AttnArgs at{};
+      at.ctl = ctl; at.qkv = m->qkv;
+      at.kc = (char*)m->kc + (size_t)l * m->kv_layer_elems * 2;
+      at.vc = (char*)m->vc + (size_t)l * m->kv_layer_elems * 2;
+      at.cos = m->w.rope_cos; at.sin = m->w.rope_sin; at.out = nullptr; at.out_b = m->attn_b; at.ldo = H * hd;
+      at.H = H; at.KV = KV; at.hd = hd; at.S = c.max_seq; at.scale = 1.0f / sqrtf((float)hd);
+      at.ws = m->attn_ws; at.counters = m->attn_cnt; at.max_splits = attn_max_splits(c.max_seq);
+      CUDA_TRY(launch_attention(c.dtype, at, st, pdl));
+      break;
+    }
+    case 2:
+      g.epi = tc::kTcResid; g.ntiles = d / 128; g.kb = H * hd / 64; g.N = d; g.out = m->h; g.ldo = d;
+      g.xnext = m->xa_b; g.gnext = (const __nv_bfloat16*)m->w.mlp_norm[l]; g.ssp = m->ssp;
+      g.wt = m->wt_o[l];
+      CUDA_TRY(tc::launch_gemm_tc(m->map_attn, g, st, pdl));
+      break;
+    case 3:
+      g.epi = tc::kTcGateUp; g.ntiles = c.ffn / 64; g.kb = d / 64; g.N = c.ffn; g.ssp_in = m->ssp;
+      g.out_b = m->act_b; g.ldo = c.ffn;
+      g.wt = m->wt_gu[l];
+      CUDA_TRY(tc::launch_gemm_tc(m->map_xa, g, st, pdl));
+      break;
+    case 4:
+      g.epi = tc::kTcResid; g.ntiles = d / 128; g.kb = c.ffn / 64; g.N = d; g.out = m->h; g.ldo = d;
+      g.xnext = m->xa_b; g.ssp = m->ssp;
+      g.gnext = (const __nv_bfloat16*)(l + 1 < c.n_layers ? m->w.attn_norm[l + 1] : m->w.final_norm);
+      g.wt = m->wt_d[l];
+      CUDA_TRY(tc::launch_gemm_tc(m->map_act, g, st, pdl));
+      break;
+    case 5:
+      g.epi = tc::kTcArgmax; g.ntiles = c.vocab / 128; g.kb = d / 64; g.N = c.vocab; g.ssp_in = m->ssp;
+      g.part = m->part; g.logits = want_logits ? m->logits : nullptr;
+      g.wt = m->wt_lm;
+      CUDA_TRY(tc::launch_gemm_tc(m->map_xa, g, st, pdl));
+      break;
+    case 6: CUDA_TRY(launch_argmax_final(ctl, m->part, c.vocab / 128, st, pdl)); break;
+    default: return fail(AMUSD_ERR_INVALID_INPUT, "unknown kernel id");
+  }
+  return AMUSD_OK;
+}
+
+static bool use_tc(const amusd_model* m, int nr) { return m->kind == 0 && m->tc && nr > 2; }
+
 // Enqueue one forward of `m` driven by control block `ctl` (rows <= nr).
 static int model_forward(amusd_model* m, StepCtl* ctl, int nr, cudaStream_t st, bool pdl, bool want_logits) {
   if (m->kind == 1) {
     CUDA_TRY(launch_hash_forward(ctl, m->chain, m->vocab, m->eos, m->exclude_eos, m->agree, m->agree_always, m->agree_thr, st));
     return AMUSD_OK;
   }
-  const amusd_tf_config& c = m->cfg;
-  const int dt = c.dtype;
-  const size_t wsz = dt == AMUSD_BF16 ? 2 : 4;
-  const int d = c.d_model, hd = c.head_dim, H = c.n_heads, KV = c.n_kv_heads;
-  const int ncols = (H + 2 * KV) * hd;
-  CUDA_TRY(launch_embed(dt, ctl, m->w.embed, m->h, d, st, pdl));
-  for (int l = 0; l < c.n_layers; ++l) {
-    GemvArgs g{};
-    g.ctl = ctl; g.eps = c.norm_eps; g.eos = c.eos_token; g.exclude_eos = c.exclude_eos;
-    // QKV (attention RMSNorm fused)
-    g.x = m->h; g.ldx = d; g.gamma = m->w.attn_norm[l]; g.W = m->w.wqkv[l]; g.N = ncols; g.K = d;
-    g.kc = gemv_kc(nr, d); g.out = m->qkv; g.ldo = ncols;
-    CUDA_TRY(launch_gemv(nr, dt, kEpiStore, g, st, pdl));
-    // attention (RoPE + KV append fused)
-    AttnArgs at{};
-    at.ctl = ctl; at.qkv = m->qkv;
-    at.kc = (char*)m->kc + (size_t)l * m->kv_layer_elems * wsz;
-    at.vc = (char*)m->vc + (size_t)l * m->kv_layer_elems * wsz;
-    at.cos = m->w.rope_cos; at.sin = m->w.rope_sin; at.out = m->attn; at.ldo = H * hd;
-    at.H = H; at.KV = KV; at.hd = hd; at.S = c.max_seq; at.scale = 1.0f / sqrtf((float)hd);
-    CUDA_TRY(launch_attention(dt, at, st, pdl));
-    // O projection + residual
-    g.x = m->attn; g.ldx = H * hd; g.gamma = nullptr; g.W = m->w.wo[l]; g.N = d; g.K = H * hd;
-    g.kc = gemv_kc(nr, H * hd); g.out = m->h; g.ldo = d;
-    CUDA_TRY(launch_gemv(nr, dt, kEpiResid, g, st, pdl));
-    // gate/up (MLP RMSNorm + SiLU*mul fused)
-    g.x = m->h; g.ldx = d; g.gamma = m->w.mlp_norm[l]; g.W = m->w.wgate[l]; g.W2 = m->w.wup[l];
-    g.N = c.ffn; g.K = d; g.kc = gemv_kc(nr, d); g.out = m->act; g.ldo = c.ffn;
-    CUDA_TRY(launch_gemv(nr, dt, kEpiGateUp, g, st, pdl));
-    // down projection + residual
-    g.x = m->act; g.ldx = c.ffn; g.gamma = nullptr; g.W = m->w.wdown[l]; g.W2 = nullptr; g.N = d;
-    g.K = c.ffn; g.kc = gemv_kc(nr, c.ffn); g.out = m->h; g.ldo = d;
-    CUDA_TRY(launch_gemv(nr, dt, kEpiResid, g, st, pdl));
+  if (use_tc(m, nr)) {
+    if (int r = tc_kernel(m, ctl, 0, 7, st, pdl)) return r;
+    for (int l = 0; l < m->cfg.n_layers; ++l)
+      for (int k = 0; k < 5; ++k)
+        if (int r = tc_kernel(m, ctl, l, k, st, pdl)) return r;
+    for (int k = 5; k < 7; ++k)
+      if (int r = tc_kernel(m, ctl, 0, k, st, pdl, want_logits)) return r;
+    return AMUSD_OK;
   }
-  GemvArgs g{};
-  g.ctl = ctl; g.eps = c.norm_eps; g.eos = c.eos_token; g.exclude_eos = c.exclude_eos;
-  g.x = m->h; g.ldx = d; g.gamma = m->w.final_norm; g.W = m->w.lm_head; g.N = c.vocab; g.K = d;
-  g.kc = gemv_kc(nr, d); g.part = m->part; g.logits = want_logits ? m->logits : nullptr;
-  CUDA_TRY(launch_gemv(nr, dt, kEpiArgmax, g, st, pdl));
-  CUDA_TRY(launch_argmax_final(ctl, m->part, m->lm_grid, st, pdl));
-  return AMUSD_OK;
+  if (int r = tf_kernel(m, ctl, nr, 0, 7, st, pdl, false)) return r;
+  for (int l = 0; l < m->cfg.n_layers; ++l)
+    for (int k = 0; k < 5; ++k)
+      if (int r = tf_kernel(m, ctl, nr, l, k, st, pdl, false)) return r;
+  if (int r = tf_kernel(m, ctl, nr, 0, 5, st, pdl, want_logits)) return r;
+  return tf_kernel(m, ctl, nr, 0, 6, st, pdl, false);
 }
 
-static int model_kernels_per_forward(const amusd_model* m) {
-  return m->kind == 1 ? 1 : 1 + 5 * m->cfg.n_layers + 2;
+static int model_kernels_per_forward(const amusd_model* m, int nr = KMAX) {
+  if (m->kind == 1) return 1;
+  if (use_tc(m, nr)) return 1 + 5 * m->cfg.n_layers + 2;
+  return 1 + 5 * m->cfg.n_layers + 2;
 }
 
 extern "C" {
@@ -193,8 +340,11 @@ int amusd_tf_create(amusd_model** out, const amusd_tf_config* cfg, const amusd_t
     return fail(AMUSD_ERR_UNSUPPORTED, "d_model, ffn and n_heads*head_dim must be multiples of 256");
   if (c.dtype != AMUSD_F32 && c.dtype != AMUSD_BF16) return fail(AMUSD_ERR_INVALID_INPUT, "bad dtype");
   if (state_bytes < amusd_tf_state_bytes(cfg)) return fail(AMUSD_ERR_INVALID_INPUT, "state buffer too small");
-  if (((size_t)c.max_seq + 2 * KMAX + 1) * sizeof(float) * 1 > 190 * 1024)
-    return fail(AMUSD_ERR_UNSUPPORTED, "max_seq too large for the attention kernel");
+  {
+    const int group = c.n_heads / c.n_kv_heads;
+    if (!(c.head_dim == 64 || c.head_dim == 128) || !(group == 2 || group == 4 || group == 8))
+      return fail(AMUSD_ERR_UNSUPPORTED, "attention kernels support head_dim 64/128 and GQA groups 2/4/8");
+  }
   amusd_model* m = new amusd_model();
   m->kind = 0;
   m->cfg = c;
@@ -204,6 +354,34 @@ int amusd_tf_create(amusd_model** out, const amusd_tf_config* cfg, const amusd_t
   m->exclude_eos = c.exclude_eos;
   m->max_seq = c.max_seq;
   tf_carve(cfg, state, m);
+  if (m->tc) {
+    const int d = c.d_model, ncols = (c.n_heads + 2 * c.n_kv_heads) * c.head_dim, hh = c.n_heads * c.head_dim;
+    bool ok = true;
+    uint8_t* p = m->tiled;
+    cudaError_t e = cudaSuccess;
+    auto place = [&](const void* src, const void* src2, int N, int K) -> const uint8_t* {
+      const uint8_t* at = p;
+      if (e == cudaSuccess) e = tc::launch_tile_weights(src, src2, p, N, K, 0);
+      p += tc::tiled_bytes(src2 ? 2 * N : N, K);
+      return at;
+    };
+    for (int l = 0; l < c.n_layers; ++l) {
+      m->wt_qkv.push_back(place(w->wqkv[l], nullptr, ncols, d));
+      m->wt_o.push_back(place(w->wo[l], nullptr, d, hh));
+      m->wt_gu.push_back(place(w->wgate[l], w->wup[l], c.ffn, d));
+      m->wt_d.push_back(place(w->wdown[l], nullptr, d, c.ffn));
+    }
+    m->wt_lm = place(w->lm_head, nullptr, c.vocab, d);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    ok &= tc::make_map(&m->map_xa, m->xa_b, KMAX, d, KMAX);
+    ok &= tc::make_map(&m->map_attn, m->attn_b, KMAX, hh, KMAX);
+    ok &= tc::make_map(&m->map_act, m->act_b, KMAX, c.ffn, KMAX);
+    if (!ok || e != cudaSuccess) {
+      delete m;
+      return fail(AMUSD_ERR_CUDA, std::string("tcgen05 path setup failed: ") +
+                                      (e != cudaSuccess ? cudaGetErrorString(e) : "cuTensorMapEncodeTiled"));
+    }
+  }
   *out = m;
   return AMUSD_OK;
 }
@@ -280,7 +458,11 @@ static int api_forward(amusd_model* m, int pos0, const int* rows_tok, int rows, 
   c.npend = rows;
   for (int i = 0; i < rows; ++i) c.tok[i] = rows_tok[i];
   CUDA_TRY(cudaMemcpyAsync(m->api_ctl, &c, sizeof(c), cudaMemcpyHostToDevice, st));
-  int r = model_forward(m, m->api_ctl, rows <= 2 ? 2 : KMAX, st, false, true);
+  // tensor-core models always run the 16-row tcgen05 forward (identical
+  // arithmetic to the engines' verify steps); SIMT models pick 2 or 16 rows,
+  // which give identical per-row results (same per-lane k order).
+  const int nr = (m->tc || rows > 2) ? KMAX : 2;
+  int r = model_forward(m, m->api_ctl, nr, st, false, true);
   if (r) return r;
   m->last_rows = rows;
   if (preds) {
@@ -676,6 +858,8 @@ int amusd_session_info(amusd_session* s, amusd_run_info* info, int32_t* V, int v
   info->acks = h.db.acks;
   info->n_draft_events = counts[0];
   info->n_verify_events = counts[1];
+  info->draft_iters = h.db.iters;
+  info->verify_iters = h.vb.iters;
   if (V && v_cap > 0) {
     const int nv = std::min(v_cap, std::max(0, h.vb.p_v - s->d.prompt_len));
     if (nv) CUDA_TRY(cudaMemcpyAsync(V, mb_V(s->mb_local, s->cap), sizeof(int) * nv, cudaMemcpyDeviceToHost, st));
@@ -698,10 +882,45 @@ int amusd_session_trace(amusd_session* s, int actor, amusd_trace_event* out, int
   return AMUSD_OK;
 }
 
+int amusd_time_forward(amusd_model* m, int rows, int which, int layer, int iters, float* ms, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!m || !ms || iters < 1) return fail(AMUSD_ERR_INVALID_INPUT, "bad argument");
+  if (rows < 1 || rows > KMAX) return fail(AMUSD_ERR_INVALID_INPUT, "rows must be in [1, 16]");
+  if (m->kind == 0 && which >= 0 && (layer < 0 || layer >= m->cfg.n_layers))
+    return fail(AMUSD_ERR_INVALID_INPUT, "layer out of range");
+  if (int r = sync_from_device(m, st)) return r;
+  const int pos0 = std::max(0, std::min(m->kv_len, m->max_seq - rows - 1));
+  StepCtl c{};
+  c.active = 1; c.rows = rows; c.pos0 = pos0; c.npend = rows;
+  for (int i = 0; i < rows; ++i) c.tok[i] = (i * 7919 + 3) % m->vocab;
+  CUDA_TRY(cudaMemcpyAsync(m->api_ctl, &c, sizeof(c), cudaMemcpyHostToDevice, st));
+  const int nr = rows <= 2 ? 2 : KMAX;
+  auto once = [&]() -> int {
+    if (which < 0 || m->kind == 1) return model_forward(m, m->api_ctl, nr, st, false, false);
+    if (use_tc(m, nr)) return tc_kernel(m, m->api_ctl, layer, which, st, false);
+    return tf_kernel(m, m->api_ctl, nr, layer, which, st, false, false);
+  };
+  if (int r = once()) return r;  // warm-up
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  CUDA_TRY(cudaEventRecord(e0, st));
+  for (int i = 0; i < iters; ++i)
+    if (int r = once()) return r;
+  CUDA_TRY(cudaEventRecord(e1, st));
+  CUDA_TRY(cudaEventSynchronize(e1));
+  float t = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&t, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *ms = t / iters;
+  return AMUSD_OK;
+}
+
 int amusd_session_kernels_per_step(amusd_session* s, int engine, int* draft_step, int* verify_step) {
   if (!s || !draft_step || !verify_step) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
-  *draft_step = s->draft ? model_kernels_per_forward(s->draft) + 2 : 0;
-  *verify_step = s->verify ? model_kernels_per_forward(s->verify) + 2 : 0;
+  *draft_step = s->draft ? model_kernels_per_forward(s->draft, 2) + 2 : 0;
+  *verify_step = s->verify ? model_kernels_per_forward(s->verify, KMAX) + 2 : 0;
   if (engine == AMUSD_ENGINE_SYNC) *verify_step += 1;
   return AMUSD_OK;
 }

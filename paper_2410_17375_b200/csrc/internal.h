@@ -22,14 +22,16 @@ struct alignas(128) MbVerifyBlock {  // written by verify, polled by draft
   int complete;       // completion flag                    coordination.py:257
   int error;          // protocol-violation word (0 = ok)
   int verify_steps, rollbacks;
-  int pad[24];
+  int iters;          // verify loop iterations (kernel-launch accounting)
+  int pad[23];
 };
 struct alignas(128) MbDraftBlock {  // written by draft, polled by verify
   int p_d;            // draft frontier (absolute)          coordination.py:136
   int rb_ack;         // rollback acknowledgment epoch      coordination.py:188
   int error;
   int drafted, acks;
-  int pad[27];
+  int iters;          // draft loop iterations (kernel-launch accounting)
+  int pad[26];
 };
 struct MailboxHdr {
   MbVerifyBlock vb;

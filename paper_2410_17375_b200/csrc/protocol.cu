@@ -85,6 +85,8 @@ __global__ void k_draft_begin(ProtoArgs a) {
   MailboxHdr* L = a.mb_local;
   MailboxHdr* R = a.mb_peer;
   c->active = 0;
+  R->db.iters += 1;
+  if (L != R) L->db.iters = R->db.iters;
   jitter(a, 0x0D, *a.dtrace.count);
   const long long t_enter = globaltimer();
   const int seq_limit = min(s->cap, a.P + a.cap) - 1;
@@ -167,6 +169,8 @@ __global__ void k_verify_begin(ProtoArgs a) {
   MailboxHdr* L = a.mb_local;
   MailboxHdr* R = a.mb_peer;
   c->active = 0;
+  R->vb.iters += 1;
+  if (L != R) L->vb.iters = R->vb.iters;
   jitter(a, 0x5E, *a.vtrace.count);
   const long long t_enter = globaltimer();
   int pd;
@@ -257,6 +261,7 @@ __global__ void k_verify_end(ProtoArgs a) {
 __global__ void k_ar_begin(ProtoArgs a) {
   if (threadIdx.x != 0) return;
   StepCtl* c = a.vctl;
+  a.mb_local->vb.iters += 1;
   SeqHdr* s = a.vseq;
   const int npend = s->len - s->kv_len;
   c->npend = npend;
@@ -298,6 +303,7 @@ __global__ void k_ar_end(ProtoArgs a) {
 __global__ void k_sync_round_begin(ProtoArgs a) {
   if (threadIdx.x != 0) return;
   StepCtl* c = a.vctl;
+  a.mb_local->vb.iters += 1;
   const int verified = a.vseq->len - a.P;
   c->kr = min(a.k, a.N - verified);  // engines.py:190-191
   c->ncand = 0;
@@ -411,8 +417,8 @@ __global__ void k_session_reset(ProtoArgs a, const int* prompt, unsigned long lo
   {  // each GPU of a split pair resets its own copy (host barrier follows)
     MailboxHdr* m = a.mb_local;
     m->vb.p_v = a.P; m->vb.rb_req = 0; m->vb.rb_target = 0; m->vb.rb_correction = 0;
-    m->vb.complete = 0; m->vb.error = 0; m->vb.verify_steps = 0; m->vb.rollbacks = 0;
-    m->db.p_d = a.P; m->db.rb_ack = 0; m->db.error = 0; m->db.drafted = 0; m->db.acks = 0;
+    m->vb.complete = 0; m->vb.error = 0; m->vb.verify_steps = 0; m->vb.rollbacks = 0; m->vb.iters = 0;
+    m->db.p_d = a.P; m->db.rb_ack = 0; m->db.error = 0; m->db.drafted = 0; m->db.acks = 0; m->db.iters = 0;
   }
   if (a.dctl) { a.dctl->rb_ack_local = 0; a.dctl->active = 0; a.dctl->t0 = globaltimer(); }
   if (a.vctl) { a.vctl->rb_ack_local = 0; a.vctl->active = 0; a.vctl->t0 = globaltimer(); }

@@ -27,12 +27,12 @@ template <typename WT>
 __global__ void k_embed(const StepCtl* __restrict__ ctl, const WT* __restrict__ emb, float* __restrict__ h,
                         int d) {
   pdl_wait();
+  pdl_launch();
   if (!ctl->active) return;
   const int r = blockIdx.x;
   if (r >= ctl->rows) return;
   const WT* src = emb + (size_t)ctl->tok[r] * d;
   for (int k = threadIdx.x; k < d; k += blockDim.x) h[(size_t)r * d + k] = Elem<WT>::to_f(src[k]);
-  pdl_launch();
 }
 
 // ------------------------------------------------------------------ gemv
@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(kGemvThreads) k_gemv(GemvArgs a) {
     }
   }
   pdl_wait();
+  pdl_launch();
   if (!a.ctl->active) return;
   const int rows = a.ctl->rows;
 
@@ -151,7 +152,6 @@ __global__ void __launch_bounds__(kGemvThreads) k_gemv(GemvArgs a) {
       }
     }
   }
-  pdl_launch();
 
   // RMSNorm scale per row (every CTA computes the same value, same order).
   float inv[NR];
@@ -217,6 +217,7 @@ __global__ void __launch_bounds__(kGemvThreads) k_gemv(GemvArgs a) {
 // Final argmax over the per-CTA partials; writes ctl->preds[r].
 __global__ void k_argmax_final(StepCtl* ctl, const unsigned long long* __restrict__ part, int nparts) {
   pdl_wait();
+  pdl_launch();
   if (!ctl->active) return;
   const int r = blockIdx.x;
   if (r >= ctl->rows) return;
@@ -234,107 +235,194 @@ __global__ void k_argmax_final(StepCtl* ctl, const unsigned long long* __restric
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = sb[w] > m ? sb[w] : m;
     ctl->preds[r] = argmax_key_index(m);
   }
-  pdl_launch();
 }
 
 // ------------------------------------------------------------- attention
-// Grid (H, KMAX).  CTA (h, r) attends row r (position p = pos0 + r) over
-// positions [0, p].  Keys/values of this step's rows come straight from the
-// QKV buffer (RoPE applied here, rounded to the cache dtype so the result is
-// identical to reading them back from the cache in a later step); the CTA of
-// the first head of each KV group also appends row r's K/V to the cache.
-template <typename WT>
+// Decode/verify attention, one CTA per (KV head g, window row r, position
+// split).  The GROUP query heads sharing KV head g are processed together so
+// K/V are read once.  Row r (position p = pos0 + r) attends [0, p]; keys and
+// values of this step's rows come from the QKV buffer (RoPE applied here,
+// rounded to the cache dtype so they equal what a later step reads back from
+// the cache); the CTA owning position p appends row r's K/V to the cache.
+// Positions are split in chunks of kAttnChunk; a row with several chunks is
+// finished by the last-arriving chunk CTA, which merges the (max, sum, acc)
+// partials in chunk order -- deterministic, and the chunking depends on the
+// position only (never on the number of rows): batch invariant.
+constexpr int kAttnChunk = 256;
+
+template <typename WT, int HD, int GROUP>
 __global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
-  extern __shared__ float sm[];
-  const int h = blockIdx.x, r = blockIdx.y;
-  const int hd = a.hd, half = hd >> 1;
-  const int group = a.H / a.KV, g = h / group;
-  float* qs = sm;                 // [hd]
-  float* kn = qs + hd;            // [KMAX][hd] this step's rotated keys
-  float* vn = kn + KMAX * hd;     // [KMAX][hd]
-  float* sc = vn + KMAX * hd;     // [S] scores
-  __shared__ float red[32];
+  constexpr int DPL = HD / 32;  // dims per lane
+  __shared__ float qs[GROUP][HD];
+  __shared__ float kn[KMAX][HD];
+  __shared__ float vn[KMAX][HD];
+  __shared__ float sc[GROUP][kAttnChunk];
+  __shared__ float red[4][GROUP][HD];
+  __shared__ float stat[2][GROUP];
+  __shared__ int s_last;
+  const int g = blockIdx.x, r = blockIdx.y, split = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_wait();
+  pdl_launch();
   if (!a.ctl->active) return;
   const int rows = a.ctl->rows, pos0 = a.ctl->pos0;
   if (r >= rows) return;
   const int p = pos0 + r;
-  const int ncols = (a.H + 2 * a.KV) * hd;
-  // rotate q (row r, head h) and the step's keys/values of group g
-  for (int i = threadIdx.x; i < half; i += blockDim.x) {
-    const float c = a.cos[(size_t)p * half + i], s = a.sin[(size_t)p * half + i];
-    const float* q = a.qkv + (size_t)r * ncols + h * hd;
-    const float x1 = q[i], x2 = q[i + half];
-    qs[i] = x1 * c - x2 * s;
-    qs[i + half] = x2 * c + x1 * s;
+  const int nsplit = (p + kAttnChunk) / kAttnChunk;  // chunks covering [0, p]
+  if (split >= nsplit) return;
+  const int lo = split * kAttnChunk, hi = min(p + 1, lo + kAttnChunk);
+  const int half = HD / 2, ncols = (a.H + 2 * a.KV) * HD;
+  // rotated queries of the group
+  for (int i = threadIdx.x; i < GROUP * half; i += blockDim.x) {
+    const int j = i / half, e = i - j * half;
+    const float* q = a.qkv + (size_t)r * ncols + (g * GROUP + j) * HD;
+    const float c = a.cos[(size_t)p * half + e], s = a.sin[(size_t)p * half + e];
+    qs[j][e] = q[e] * c - q[e + half] * s;
+    qs[j][e + half] = q[e + half] * c + q[e] * s;
   }
-  for (int j = 0; j <= r; ++j) {
+  // this step's keys/values for rows 0..r, only if the chunk reaches pos0
+  const int jmax = hi > pos0 ? min(r, hi - 1 - pos0) : -1;
+  for (int i = threadIdx.x; i < (jmax + 1) * half; i += blockDim.x) {
+    const int j = i / half, e = i - j * half;
     const int pj = pos0 + j;
-    const float* kr = a.qkv + (size_t)j * ncols + (a.H + g) * hd;
-    const float* vr = a.qkv + (size_t)j * ncols + (a.H + a.KV + g) * hd;
-    for (int i = threadIdx.x; i < half; i += blockDim.x) {
-      const float c = a.cos[(size_t)pj * half + i], s = a.sin[(size_t)pj * half + i];
-      const float x1 = kr[i], x2 = kr[i + half];
-      kn[j * hd + i] = Elem<WT>::to_f(Elem<WT>::from_f(x1 * c - x2 * s));
-      kn[j * hd + i + half] = Elem<WT>::to_f(Elem<WT>::from_f(x2 * c + x1 * s));
-    }
-    for (int i = threadIdx.x; i < hd; i += blockDim.x) vn[j * hd + i] = Elem<WT>::to_f(Elem<WT>::from_f(vr[i]));
+    const float* kr = a.qkv + (size_t)j * ncols + (a.H + g) * HD;
+    const float c = a.cos[(size_t)pj * half + e], s = a.sin[(size_t)pj * half + e];
+    kn[j][e] = Elem<WT>::to_f(Elem<WT>::from_f(kr[e] * c - kr[e + half] * s));
+    kn[j][e + half] = Elem<WT>::to_f(Elem<WT>::from_f(kr[e + half] * c + kr[e] * s));
+  }
+  for (int i = threadIdx.x; i < (jmax + 1) * HD; i += blockDim.x) {
+    const int j = i / HD, e = i - j * HD;
+    vn[j][e] = Elem<WT>::to_f(Elem<WT>::from_f(a.qkv[(size_t)j * ncols + (a.H + a.KV + g) * HD + e]));
   }
   __syncthreads();
-  WT* kc = (WT*)a.kc + (size_t)g * a.S * hd;
-  WT* vc = (WT*)a.vc + (size_t)g * a.S * hd;
-  if (h % group == 0) {  // append row r's K/V (KV-cache write, pending-token scheme)
-    for (int i = threadIdx.x; i < hd; i += blockDim.x) {
-      kc[(size_t)p * hd + i] = Elem<WT>::from_f(kn[r * hd + i]);
-      vc[(size_t)p * hd + i] = Elem<WT>::from_f(vn[r * hd + i]);
+  WT* kc = (WT*)a.kc + (size_t)g * a.S * HD;
+  WT* vc = (WT*)a.vc + (size_t)g * a.S * HD;
+  if (p >= lo && p < hi) {  // KV append for row r (pending-token scheme)
+    for (int e = threadIdx.x; e < HD; e += blockDim.x) {
+      kc[(size_t)p * HD + e] = Elem<WT>::from_f(kn[r][e]);
+      vc[(size_t)p * HD + e] = Elem<WT>::from_f(vn[r][e]);
     }
   }
-  // scores
-  float mx = -INFINITY;
-  for (int t = threadIdx.x; t <= p; t += blockDim.x) {
-    float dot = 0.f;
-    if (t < pos0) {
-      const WT* kt = kc + (size_t)t * hd;
-      for (int i = 0; i < hd; i += Elem<WT>::kVec) {
-        float f[Elem<WT>::kVec];
-        Elem<WT>::unpack(*(const uint4*)(kt + i), f);
+  // scores: warp w takes positions lo+w, lo+w+4, ...; lane holds DPL dims
+  float qreg[GROUP][DPL];
 #pragma unroll
-        for (int e = 0; e < Elem<WT>::kVec; ++e) dot = fmaf(qs[i + e], f[e], dot);
-      }
+  for (int j = 0; j < GROUP; ++j)
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) qreg[j][e] = qs[j][lane * DPL + e];
+  for (int t = lo + warp; t < hi; t += 4) {
+    float kv[DPL];
+    if (t < pos0) {
+      const WT* kt = kc + (size_t)t * HD + lane * DPL;
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) kv[e] = Elem<WT>::to_f(kt[e]);
     } else {
-      const float* kt = kn + (t - pos0) * hd;
-      for (int i = 0; i < hd; ++i) dot = fmaf(qs[i], kt[i], dot);
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) kv[e] = kn[t - pos0][lane * DPL + e];
     }
-    dot *= a.scale;
-    sc[t] = dot;
-    mx = fmaxf(mx, dot);
+#pragma unroll
+    for (int j = 0; j < GROUP; ++j) {
+      float d = 0.f;
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) d = fmaf(qreg[j][e], kv[e], d);
+      d = warp_sum(d);
+      if (lane == 0) sc[j][t - lo] = d * a.scale;
+    }
   }
-  mx = warp_max(mx);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
   __syncthreads();
-  mx = red[0];
-  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmaxf(mx, red[w]);
-  __syncthreads();
-  float sum = 0.f;
-  for (int t = threadIdx.x; t <= p; t += blockDim.x) {
-    const float e = expf(sc[t] - mx);
-    sc[t] = e;
-    sum += e;
+  // per-head max and exp-sum over this chunk (one warp per head, fixed order)
+  for (int j = warp; j < GROUP; j += 4) {
+    float m = -INFINITY;
+    for (int t = lane; t < hi - lo; t += 32) m = fmaxf(m, sc[j][t]);
+    m = warp_max(m);
+    float l = 0.f;
+    for (int t = lane; t < hi - lo; t += 32) {
+      const float e = expf(sc[j][t] - m);
+      sc[j][t] = e;
+      l += e;
+    }
+    l = warp_sum(l);
+    if (lane == 0) { stat[0][j] = m; stat[1][j] = l; }
   }
-  sum = warp_sum(sum);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
   __syncthreads();
-  sum = 0.f;
-  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) sum += red[w];
-  const float inv = 1.f / sum;
-  for (int i = threadIdx.x; i < hd; i += blockDim.x) {
-    float o = 0.f;
-    for (int t = 0; t < pos0 && t <= p; ++t) o = fmaf(sc[t], Elem<WT>::to_f(vc[(size_t)t * hd + i]), o);
-    for (int t = pos0; t <= p; ++t) o = fmaf(sc[t], vn[(t - pos0) * hd + i], o);
-    a.out[(size_t)r * a.ldo + h * hd + i] = o * inv;
+  // unnormalised output: warp w takes positions lo+w, lo+w+4, ...
+  float acc[GROUP][DPL];
+#pragma unroll
+  for (int j = 0; j < GROUP; ++j)
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) acc[j][e] = 0.f;
+  for (int t = lo + warp; t < hi; t += 4) {
+    float vv[DPL];
+    if (t < pos0) {
+      const WT* vt = vc + (size_t)t * HD + lane * DPL;
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) vv[e] = Elem<WT>::to_f(vt[e]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) vv[e] = vn[t - pos0][lane * DPL + e];
+    }
+#pragma unroll
+    for (int j = 0; j < GROUP; ++j) {
+      const float pj = sc[j][t - lo];
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) acc[j][e] = fmaf(pj, vv[e], acc[j][e]);
+    }
   }
-  pdl_launch();
+#pragma unroll
+  for (int j = 0; j < GROUP; ++j)
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) red[warp][j][lane * DPL + e] = acc[j][e];
+  __syncthreads();
+  auto emit = [&](int j, int e, float o) {
+    const size_t idx = (size_t)r * a.ldo + (g * GROUP + j) * HD + e;
+    if (a.out_b) ((__nv_bfloat16*)a.out_b)[idx] = __float2bfloat16(o);
+    else a.out[idx] = o;
+  };
+  if (nsplit == 1) {
+    for (int i = threadIdx.x; i < GROUP * HD; i += blockDim.x) {
+      const int j = i / HD, e = i - j * HD;
+      const float o = red[0][j][e] + red[1][j][e] + red[2][j][e] + red[3][j][e];
+      emit(j, e, o / stat[1][j]);
+    }
+    return;
+  }
+  // multi-chunk row: park the partial, the last chunk CTA merges in chunk order
+  float* ws = a.ws + (((size_t)g * KMAX + r) * a.max_splits + split) * GROUP * (HD + 2);
+  for (int i = threadIdx.x; i < GROUP * HD; i += blockDim.x) {
+    const int j = i / HD, e = i - j * HD;
+    ws[j * (HD + 2) + e] = red[0][j][e] + red[1][j][e] + red[2][j][e] + red[3][j][e];
+  }
+  if (threadIdx.x < GROUP) {
+    ws[threadIdx.x * (HD + 2) + HD] = stat[0][threadIdx.x];
+    ws[threadIdx.x * (HD + 2) + HD + 1] = stat[1][threadIdx.x];
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int* cnt = a.counters + g * KMAX + r;
+    const int old = atomicAdd(cnt, 1);
+    s_last = (old == nsplit - 1);
+    if (s_last) *cnt = 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const float* base = a.ws + ((size_t)g * KMAX + r) * a.max_splits * GROUP * (HD + 2);
+  for (int i = threadIdx.x; i < GROUP * HD; i += blockDim.x) {
+    const int j = i / HD, e = i - j * HD;
+    float M = -INFINITY;
+    for (int s2 = 0; s2 < nsplit; ++s2) M = fmaxf(M, __ldcg(base + ((size_t)s2 * GROUP + j) * (HD + 2) + HD));
+    float L = 0.f, O = 0.f;
+    for (int s2 = 0; s2 < nsplit; ++s2) {
+      const float* w = base + ((size_t)s2 * GROUP + j) * (HD + 2);
+      const float f = expf(__ldcg(w + HD) - M);
+      L += __ldcg(w + HD + 1) * f;
+      O += __ldcg(w + e) * f;
+    }
+    emit(j, e, O / L);
+  }
 }
+
+int attn_max_splits(int max_seq) { return (max_seq + kAttnChunk - 1) / kAttnChunk; }
 
 // ----------------------------------------------------------- launchers
 template <typename F, typename... Args>
@@ -397,16 +485,20 @@ cudaError_t launch_embed(int dtype, const StepCtl* ctl, const void* emb, float* 
   return launch_pdl(k_embed<float>, dim3(KMAX), dim3(256), 0, st, pdl, ctl, (const float*)emb, h, d);
 }
 
+template <typename WT>
+static cudaError_t attention_dispatch(const AttnArgs& a, cudaStream_t st, bool pdl) {
+  const dim3 grid(a.KV, KMAX, attn_max_splits(a.S));
+  const int group = a.H / a.KV;
+#define AMUSD_ATTN(HD_, G_) \
+  if (a.hd == HD_ && group == G_) return launch_pdl(k_attention<WT, HD_, G_>, grid, dim3(128), 0, st, pdl, a);
+  AMUSD_ATTN(64, 2) AMUSD_ATTN(64, 4) AMUSD_ATTN(64, 8) AMUSD_ATTN(128, 2) AMUSD_ATTN(128, 4) AMUSD_ATTN(128, 8)
+#undef AMUSD_ATTN
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_attention(int dtype, const AttnArgs& a, cudaStream_t st, bool pdl) {
-  const size_t smem = (size_t)(a.hd + 2 * KMAX * a.hd + a.S) * sizeof(float);
-  if (dtype == AMUSD_BF16) {
-    auto k = k_attention<__nv_bfloat16>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    return launch_pdl(k, dim3(a.H, KMAX), dim3(128), smem, st, pdl, a);
-  }
-  auto k = k_attention<float>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  return launch_pdl(k, dim3(a.H, KMAX), dim3(128), smem, st, pdl, a);
+  if (dtype == AMUSD_BF16) return attention_dispatch<__nv_bfloat16>(a, st, pdl);
+  return attention_dispatch<float>(a, st, pdl);
 }
 
 cudaError_t launch_argmax_final(StepCtl* ctl, const unsigned long long* part, int nparts, cudaStream_t st, bool pdl) {

@@ -31,11 +31,17 @@ struct AttnArgs {
   void* vc;                // this layer's V cache [KV][S][hd]
   const float* cos;        // [S][hd/2]
   const float* sin;
-  float* out;              // [KMAX][ldo]
+  float* out;              // [KMAX][ldo] fp32 (SIMT path)
+  void* out_b;             // [KMAX][ldo] bf16 (tensor-core path) -- used when non-null
   int ldo;
   int H, KV, hd, S;
   float scale;
+  float* ws;               // split partials [KV][KMAX][max_splits][group][hd+2]
+  int* counters;           // [KV][KMAX] arrival counters (self re-arming)
+  int max_splits;
 };
+
+int attn_max_splits(int max_seq);
 
 int gemv_kc(int nr, int K);
 int gemv_grid(int N, int rpw);
