@@ -770,7 +770,9 @@ static int capture_body(amusd_session* s, int engine, int actor, cudaGraph_t bod
   cudaStream_t st = s->capture;
   CUDA_TRY(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   int r = AMUSD_OK;
-  const bool pdl = s->use_pdl;
+  // Co-located AMUSD: early-launched (PDL) verify CTAs would hold the second
+  // SM slot and starve the draft stream -- measured 146 vs 221 tok/s on B200.
+  const bool pdl = s->use_pdl && engine != AMUSD_ENGINE_ASYNC;
   auto fwd = [&](amusd_model* m, StepCtl* c, int nr) { if (!r) r = model_forward(m, c, nr, st, pdl, false); };
   auto pk = [&](int which, int arg) { if (!r && proto_launch(which, a, st, arg) != cudaSuccess) r = fail(AMUSD_ERR_CUDA, "protocol launch failed"); };
   if (engine == AMUSD_ENGINE_AUTOREGRESSIVE) {

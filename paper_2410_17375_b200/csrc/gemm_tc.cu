@@ -558,8 +558,14 @@ int tc_grid(int ntiles, int kb) {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) g_num_sms = 148;
   }
+  static int cap = -1;
+  if (cap < 0) {  // AMUSD_TC_GRID: leave SMs to a co-located draft (scheduling knob)
+    const char* e = getenv("AMUSD_TC_GRID");
+    cap = e ? atoi(e) : 0;
+  }
+  const int sms = cap > 0 && cap < g_num_sms ? cap : g_num_sms;
   const long long U = (long long)ntiles * kb;
-  return (int)(U < g_num_sms ? U : g_num_sms);
+  return (int)(U < sms ? U : sms);
 }
 
 cudaError_t launch_gemm_tc(const CUtensorMap& mx, const TcArgs& a, cudaStream_t st, bool pdl) {

@@ -96,11 +96,17 @@ _STREAMS: dict = {}
 
 
 def streams(device) -> tuple:
-    """(verify_stream, draft_stream) for a device; verify gets the higher priority."""
+    """(verify_stream, draft_stream) for a device.
+
+    AMUSD_STREAM_PRIO = equal (default) | verify_high | draft_high.  Purely a
+    scheduling knob for the co-located pair (never changes tokens)."""
     key = torch.device(device).index or 0
     if key not in _STREAMS:
+        import os
+        mode = os.environ.get("AMUSD_STREAM_PRIO", "equal")
+        pv, pd = {"verify_high": (-1, 0), "draft_high": (0, -1)}.get(mode, (0, 0))
         with torch.cuda.device(key):
-            _STREAMS[key] = (torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=0))
+            _STREAMS[key] = (torch.cuda.Stream(priority=pv), torch.cuda.Stream(priority=pd))
     return _STREAMS[key]
 
 
