@@ -104,6 +104,17 @@ int amusd_hash_create(amusd_model** out, uint64_t seed, int vocab, int eos_token
 
 int amusd_model_destroy(amusd_model* m);
 
+/* Forward implementation of a bf16 tensor-core-shaped transformer (perf A/B
+ * and parity tests; not in the reference, whose models are Python mocks):
+ * 0 = persistent tcgen05 forward (default, one launch per forward),
+ * 1 = per-kernel tcgen05 path (1 + 5L + 2 launches), 2 = SIMT GEMV path.
+ * Applies to launches enqueued afterwards (sessions capture it per engine). */
+enum { AMUSD_PATH_PERSISTENT = 0, AMUSD_PATH_KERNELS = 1, AMUSD_PATH_SIMT = 2 };
+int amusd_model_set_path(amusd_model* m, int path);
+/* Perf analysis only: record a per-work-item timeline of the persistent
+ * forward into a device buffer (64 bytes per item; NULL disables). */
+int amusd_model_set_timeline(amusd_model* m, void* buf, size_t bytes);
+
 /* MockModel interface (models.py:85-200): synchronous on `stream`, host token
  * buffers.  Used by the parity path; the decode loops below never call it. */
 int amusd_init_state(amusd_model* m, const int32_t* prompt, int n, void* stream);       /* models.py:109 */

@@ -37,6 +37,9 @@ class TfWeights(C.Structure):
         (n, C.c_void_p * MAX_LAYERS) for n in ("attn_norm", "wqkv", "wo", "mlp_norm", "wgate", "wup", "wdown")]
 
 
+PATH_PERSISTENT, PATH_KERNELS, PATH_SIMT = 0, 1, 2  # amusd_model_set_path
+
+
 class SessionDesc(C.Structure):
     _fields_ = [("prompt_len", C.c_int), ("max_new_tokens", C.c_int), ("draft_window_k", C.c_int),
                 ("max_draft_lead", C.c_int), ("max_window", C.c_int), ("coin_mode", C.c_int),
@@ -65,6 +68,8 @@ SIGNATURES = [
     ("amusd_hash_state_bytes", _SZ, [_I]),
     ("amusd_hash_create", _I, [_P(_VP), C.c_uint64, _I, _I, _I, C.c_double, _I, _VP, _SZ]),
     ("amusd_model_destroy", _I, [_VP]),
+    ("amusd_model_set_path", _I, [_VP, _I]),
+    ("amusd_model_set_timeline", _I, [_VP, _VP, _SZ]),
     ("amusd_init_state", _I, [_VP, _P(C.c_int32), _I, _VP]),
     ("amusd_next_token", _I, [_VP, _P(C.c_int32), _VP]),
     ("amusd_advance", _I, [_VP, _P(C.c_int32), _I, _VP]),

@@ -19,6 +19,7 @@
 #include "protocol.h"
 #include "transformer.h"
 #include "gemm_tc.h"
+#include "forward_tc.h"
 
 using namespace amusd;
 
@@ -97,13 +98,70 @@ struct amusd_model {
   const uint8_t* wt_lm = nullptr;
   uint8_t* tiled = nullptr;
   CUtensorMap map_xa{}, map_attn{}, map_act{};
+  // persistent forward (forward_tc.cu): phase table + self-resetting schedule
+  fw::FwArgs fw_args{};           // schedule (GEMM kinds) + model pointers, built at create
+  bool fw_ready = false;
+  __nv_bfloat16* fw_norms = nullptr;  // packed RMSNorm weights [2L+1][d]
+  float* fw_attn_ws = nullptr;        // attention split partials (128-position chunks)
+  int* fw_attn_cnt = nullptr;
+  int* fw_sched = nullptr;
+  unsigned long long* fw_best = nullptr;
+  float* fw_ws = nullptr;
+  int* fw_tile_cnt = nullptr;
+  int fw_grid = 0, fw_stages = 0;  // launch shape (set per engine at graph capture)
+  int path = AMUSD_PATH_PERSISTENT;
+  long long* fw_dbg = nullptr;  // optional per-item timeline (amusd_model_set_timeline)
+  int fw_dbg_items = 0;
 };
+
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return (e && *e) ? atoi(e) : dflt;
+}
+// AMUSD_FW=0 selects the per-kernel tcgen05 path (A/B comparisons only).
+static bool fw_enabled() {
+  static int v = -1;
+  if (v < 0) v = env_int("AMUSD_FW", 1) != 0;
+  return v;
+}
+static int fw_units() {
+  static int v = -1;
+  if (v < 0) v = std::max(1, env_int("AMUSD_FW_UNITS", 8));
+  return v;
+}
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+// Deepest weight ring that fits `per_sm` CTAs on one SM (227 KB smem per SM).
+static int fw_max_stages(const amusd_tf_config& c, int per_sm) {
+  const int group = c.n_heads / c.n_kv_heads;
+  const int budget = (per_sm == 1 ? 232448 : 233472 / per_sm - 1024);
+  int s = 2;
+  while (s < 16 && fw::forward_smem_bytes(s + 1, c.head_dim, group) <= budget) ++s;
+  return s;
+}
 
 static bool tc_shapes_ok(const amusd_tf_config* c) {
   const int ncols = (c->n_heads + 2 * c->n_kv_heads) * c->head_dim;
   // tcgen05 tiles: 128 weight rows (64 gate + 64 up features) x 64 K per unit
   return c->dtype == AMUSD_BF16 && c->use_tensor_cores && c->d_model % 128 == 0 && ncols % 128 == 0 &&
          c->ffn % 64 == 0 && c->vocab % 128 == 0 && (c->n_heads * c->head_dim) % 64 == 0;
+}
+
+// Split-K workspace sizes of a config (dry run of build_kinds without pointers).
+static void fw_sizes(const amusd_tf_config* c, size_t* ws_floats, int* max_tiles) {
+  fw::ModelView v{};
+  v.d = c->d_model; v.H = c->n_heads; v.KV = c->n_kv_heads; v.hd = c->head_dim; v.ffn = c->ffn; v.vocab = c->vocab;
+  v.L = c->n_layers; v.S = c->max_seq;
+  fw::FwArgs a{};
+  fw::build_kinds(v, fw_units(), &a, ws_floats, max_tiles);
 }
 
 static size_t tf_carve(const amusd_tf_config* c, void* base, amusd_model* m) {
@@ -145,8 +203,29 @@ static size_t tf_carve(const amusd_tf_config* c, void* base, amusd_model* m) {
                              tc::tiled_bytes(2 * c->ffn, c->d_model) + tc::tiled_bytes(c->d_model, c->ffn);
     tiled = cv.take<uint8_t>(per_layer * c->n_layers + tc::tiled_bytes(c->vocab, c->d_model));
   }
+  int* fsched = nullptr;
+  unsigned long long* fbest = nullptr;
+  float* fws = nullptr;
+  int* fcnt = nullptr;
+  __nv_bfloat16* fnorms = nullptr;
+  float* fattn_ws = nullptr;
+  int* fattn_cnt = nullptr;
+  if (tc) {
+    int mt;
+    size_t wsf;
+    fw_sizes(c, &wsf, &mt);
+    fsched = cv.take<int>((size_t)(2 + fw::num_phases(c->n_layers)) * fw::kCounterInts);
+    fbest = cv.take<unsigned long long>(KMAX);
+    fws = cv.take<float>(std::max<size_t>(wsf, 1));
+    fcnt = cv.take<int>((size_t)std::max(mt, 1) * fw::kCounterInts);
+    fnorms = cv.take<__nv_bfloat16>((size_t)(2 * c->n_layers + 1) * c->d_model);
+    fattn_ws = cv.take<float>((size_t)c->n_kv_heads * KMAX * fw::attn_splits(c->max_seq) * group * (c->head_dim + 2));
+    fattn_cnt = cv.take<int>((size_t)c->n_kv_heads * KMAX * fw::kCounterInts);
+  }
   if (m) {
     m->attn_ws = attn_ws; m->attn_cnt = attn_cnt;
+    m->fw_sched = fsched; m->fw_best = fbest; m->fw_ws = fws; m->fw_tile_cnt = fcnt; m->fw_norms = fnorms;
+    m->fw_attn_ws = fattn_ws; m->fw_attn_cnt = fattn_cnt;
     m->tc = tc; m->xa_b = xa_b; m->attn_b = attn_b; m->act_b = act_b; m->inv = inv; m->ssp = ssp_b; m->tc_ws = ws; m->tc_cnt = cnt; m->tiled = tiled;
     m->seq = seq; m->tok = tok; m->api_ctl = ctl; m->kc = kc; m->vc = vc; m->h = h; m->qkv = qkv;
     m->attn = attn; m->act = act; m->part = part; m->logits = logits; m->lm_grid = lm_grid;
@@ -288,7 +367,35 @@ static int tc_kernel(amusd_model* m, StepCtl* ctl, int l, int which, cudaStream_
   return AMUSD_OK;
 }
 
-static bool use_tc(const amusd_model* m, int nr) { return m->kind == 0 && m->tc && nr > 2; }
+static bool use_fw(const amusd_model* m) {
+  return m->kind == 0 && m->tc && m->fw_ready && fw_enabled() && m->path == AMUSD_PATH_PERSISTENT;
+}
+// Per-kernel tcgen05 path for 16-row forwards (2-row draft steps take the SIMT GEMVs).
+static bool use_tc(const amusd_model* m, int nr) {
+  return m->kind == 0 && m->tc && nr > 2 && m->path != AMUSD_PATH_SIMT;
+}
+
+// The whole forward as one persistent launch (forward_tc.cu).
+static int fw_forward(amusd_model* m, StepCtl* ctl, cudaStream_t st, bool want_logits) {
+  const amusd_tf_config& c = m->cfg;
+  fw::FwArgs a = m->fw_args;
+  a.ctl = ctl; a.sched = m->fw_sched;
+  a.embed = (const __nv_bfloat16*)m->w.embed; a.norms = m->fw_norms;
+  a.h = m->h; a.xa = m->xa_b; a.ssp = m->ssp; a.qkv = m->qkv; a.attn_b = m->attn_b;
+  a.kcache = (char*)m->kc; a.vcache = (char*)m->vc; a.kv_layer_bytes = (long long)m->kv_layer_elems * 2;
+  a.ws = m->fw_ws; a.tile_cnt = m->fw_tile_cnt; a.attn_ws = m->fw_attn_ws; a.attn_cnt = m->fw_attn_cnt;
+  a.cos = m->w.rope_cos; a.sin = m->w.rope_sin; a.best = m->fw_best; a.logits = want_logits ? m->logits : nullptr;
+  a.d = c.d_model; a.H = c.n_heads; a.KV = c.n_kv_heads; a.hd = c.head_dim; a.S = c.max_seq;
+  a.max_splits = fw::attn_splits(c.max_seq); a.vocab = c.vocab; a.eos = c.eos_token; a.exclude_eos = c.exclude_eos;
+  a.scale = 1.0f / sqrtf((float)c.head_dim); a.eps = c.norm_eps;
+  a.dbg = m->fw_dbg; a.dbg_items = m->fw_dbg_items;
+  // L2 prefetch window (bytes of weights ahead of the grab pointer), AMUSD_FW_L2_MB
+  a.prefetch_items = (int)((size_t)env_int("AMUSD_FW_L2_MB", 0) * (1 << 20) / ((size_t)fw_units() * 16384));
+  a.inflight = env_int("AMUSD_FW_INFLIGHT", 0);
+  a.debug = env_int("AMUSD_FW_DEBUG", 0);
+  CUDA_TRY(fw::launch_forward(a, m->map_xa, m->map_attn, m->map_act, m->fw_grid, m->fw_stages, st));
+  return AMUSD_OK;
+}
 
 // Enqueue one forward of `m` driven by control block `ctl` (rows <= nr).
 static int model_forward(amusd_model* m, StepCtl* ctl, int nr, cudaStream_t st, bool pdl, bool want_logits) {
@@ -296,6 +403,7 @@ static int model_forward(amusd_model* m, StepCtl* ctl, int nr, cudaStream_t st, 
     CUDA_TRY(launch_hash_forward(ctl, m->chain, m->vocab, m->eos, m->exclude_eos, m->agree, m->agree_always, m->agree_thr, st));
     return AMUSD_OK;
   }
+  if (use_fw(m)) return fw_forward(m, ctl, st, want_logits);
   if (use_tc(m, nr)) {
     if (int r = tc_kernel(m, ctl, 0, 7, st, pdl)) return r;
     for (int l = 0; l < m->cfg.n_layers; ++l)
@@ -315,6 +423,7 @@ static int model_forward(amusd_model* m, StepCtl* ctl, int nr, cudaStream_t st, 
 
 static int model_kernels_per_forward(const amusd_model* m, int nr = KMAX) {
   if (m->kind == 1) return 1;
+  if (use_fw(m)) return 1;
   if (use_tc(m, nr)) return 1 + 5 * m->cfg.n_layers + 2;
   return 1 + 5 * m->cfg.n_layers + 2;
 }
@@ -372,6 +481,29 @@ int amusd_tf_create(amusd_model** out, const amusd_tf_config* cfg, const amusd_t
       m->wt_d.push_back(place(w->wdown[l], nullptr, d, c.ffn));
     }
     m->wt_lm = place(w->lm_head, nullptr, c.vocab, d);
+    if (e == cudaSuccess) {  // persistent forward: packed norms + GEMM kinds (kernel parameters)
+      const size_t dbytes = (size_t)d * 2;
+      for (int l = 0; l < c.n_layers && e == cudaSuccess; ++l) {
+        e = cudaMemcpy(m->fw_norms + (size_t)(2 * l) * d, w->attn_norm[l], dbytes, cudaMemcpyDeviceToDevice);
+        if (e == cudaSuccess)
+          e = cudaMemcpy(m->fw_norms + (size_t)(2 * l + 1) * d, w->mlp_norm[l], dbytes, cudaMemcpyDeviceToDevice);
+      }
+      if (e == cudaSuccess)
+        e = cudaMemcpy(m->fw_norms + (size_t)(2 * c.n_layers) * d, w->final_norm, dbytes, cudaMemcpyDeviceToDevice);
+      fw::ModelView v{};
+      v.d = d; v.H = c.n_heads; v.KV = c.n_kv_heads; v.hd = c.head_dim; v.ffn = c.ffn; v.vocab = c.vocab;
+      v.L = c.n_layers; v.S = c.max_seq;
+      v.wt_layer0 = m->wt_qkv[0];
+      v.wt_layer_bytes = c.n_layers > 1 ? (long long)(m->wt_qkv[1] - m->wt_qkv[0]) : 0;
+      v.wt_lm = m->wt_lm; v.norms = m->fw_norms;
+      v.h = m->h; v.qkv = m->qkv; v.xa = m->xa_b; v.act_b = m->act_b;
+      size_t wsf;
+      int mt;
+      fw::build_kinds(v, fw_units(), &m->fw_args, &wsf, &mt);
+      m->fw_ready = e == cudaSuccess;
+      m->fw_grid = num_sms();
+      m->fw_stages = env_int("AMUSD_FW_STAGES", fw_max_stages(c, 1));
+    }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     ok &= tc::make_map(&m->map_xa, m->xa_b, KMAX, d, KMAX);
     ok &= tc::make_map(&m->map_attn, m->attn_b, KMAX, hh, KMAX);
@@ -416,6 +548,24 @@ int amusd_hash_create(amusd_model** out, uint64_t seed, int vocab, int eos, int 
 
 int amusd_model_destroy(amusd_model* m) {
   delete m;
+  return AMUSD_OK;
+}
+
+int amusd_model_set_timeline(amusd_model* m, void* buf, size_t bytes) {
+  if (!m) return fail(AMUSD_ERR_INVALID_INPUT, "null model");
+  m->fw_dbg = (long long*)buf;
+  m->fw_dbg_items = buf ? (int)std::min<size_t>(bytes / 64, 1 << 20) : 0;
+  return AMUSD_OK;
+}
+
+int amusd_model_set_path(amusd_model* m, int path) {
+  if (!m) return fail(AMUSD_ERR_INVALID_INPUT, "null model");
+  if (path < AMUSD_PATH_PERSISTENT || path > AMUSD_PATH_SIMT) return fail(AMUSD_ERR_INVALID_INPUT, "unknown path");
+  if (path != AMUSD_PATH_SIMT && m->kind == 0 && !m->tc)
+    return fail(AMUSD_ERR_UNSUPPORTED, "tensor-core paths need a bf16 model with 128-aligned shapes");
+  if (m->kind == 0 && m->cfg.dtype == AMUSD_BF16 && path == AMUSD_PATH_SIMT && !m->w.wgate[0])
+    return fail(AMUSD_ERR_UNSUPPORTED, "SIMT path needs row-major weights");
+  m->path = path;
   return AMUSD_OK;
 }
 
@@ -773,6 +923,18 @@ static int capture_body(amusd_session* s, int engine, int actor, cudaGraph_t bod
   // Co-located AMUSD: early-launched (PDL) verify CTAs would hold the second
   // SM slot and starve the draft stream -- measured 146 vs 221 tok/s on B200.
   const bool pdl = s->use_pdl && engine != AMUSD_ENGINE_ASYNC;
+  // Persistent-forward launch shape: co-located AMUSD runs the draft and the
+  // verify forward at the same time, so each gets a ring that lets two CTAs
+  // share an SM; every other engine owns the GPU (deepest ring, 1 CTA/SM).
+  const bool colo = engine == AMUSD_ENGINE_ASYNC;
+  for (amusd_model* m : {s->draft, s->verify}) {
+    if (!m || !use_fw(m)) continue;
+    m->fw_stages = colo ? env_int("AMUSD_FW_COLO_STAGES", fw_max_stages(m->cfg, 2))
+                        : env_int("AMUSD_FW_STAGES", fw_max_stages(m->cfg, 1));
+    m->fw_grid = num_sms();
+    if (colo && m == s->draft) m->fw_grid = std::max(1, std::min(num_sms(), env_int("AMUSD_FW_DRAFT_GRID", num_sms())));
+    if (colo && m == s->verify) m->fw_grid = std::max(1, std::min(num_sms(), env_int("AMUSD_FW_VERIFY_GRID", num_sms())));
+  }
   auto fwd = [&](amusd_model* m, StepCtl* c, int nr) { if (!r) r = model_forward(m, c, nr, st, pdl, false); };
   auto pk = [&](int which, int arg) { if (!r && proto_launch(which, a, st, arg) != cudaSuccess) r = fail(AMUSD_ERR_CUDA, "protocol launch failed"); };
   if (engine == AMUSD_ENGINE_AUTOREGRESSIVE) {
@@ -790,6 +952,11 @@ static int capture_body(amusd_session* s, int engine, int actor, cudaGraph_t bod
   }
   cudaGraph_t g2 = body;
   cudaError_t e = cudaStreamEndCapture(st, &g2);
+  for (amusd_model* m : {s->draft, s->verify}) {  // parity API launches own the GPU again
+    if (!m || !use_fw(m)) continue;
+    m->fw_stages = env_int("AMUSD_FW_STAGES", fw_max_stages(m->cfg, 1));
+    m->fw_grid = num_sms();
+  }
   if (r) return r;
   CUDA_TRY(e);
   return AMUSD_OK;

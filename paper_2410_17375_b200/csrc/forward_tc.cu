@@ -1,0 +1,1033 @@
+// forward_tc.cu -- persistent tcgen05 decoder forward (SURVEY.md K2 + K4).
+//
+// One launch runs a whole forward of the Llama-style model over <= 16 token
+// rows (the draft's pending token, the verify window).  The forward is a list
+// of phases -- embed, then per layer QKV GEMM / attention / O GEMM / gate-up
+// GEMM / down GEMM, then the LM-head GEMM with the greedy argmax -- cut into
+// work items that CTAs grab from one global counter in phase order.
+//
+// Why a work queue rather than one kernel per GEMM: a decode forward is a
+// stream of 2.5 GB (1B) / 15 GB (8B) of weights with a dependency every few
+// tens of MB.  Weights never depend on activations, so a CTA that grabbed an
+// item of phase p+1 streams that item's weights into its shared-memory ring
+// right away and waits for phase p only before loading the activation tile
+// (X) and issuing the MMAs.  HBM stays busy across the layer's dependency
+// chain instead of draining at every kernel boundary.  Items are grabbed in
+// global order, so every item a CTA waits on was grabbed by a CTA that is
+// already running: forward progress never needs co-residency, and a draft
+// forward and a verify forward can share the GPU (co-located AMUSD).
+//
+// Warp roles (320 threads):
+//   w0      scheduler + weight producer (1-D bulk copies, 16 KB per unit)
+//   w1      activation loader: waits for the dependency, then X tiles by TMA
+//   w2..w5  tcgen05.mma issuers: warp w issues K-slice w-2 of every unit into
+//           its own TMEM accumulator chain (issue-rate bound)
+//   w6..w9  epilogue (TMEM -> registers -> fused epilogue) and the SIMT items
+//           (embedding, attention)
+// The roles follow the same item sequence through a 4-deep shared-memory
+// queue; weight/X stages and the TMEM double buffer are mbarrier rings.
+//
+// Determinism / batch invariance: split-K partials of a tile are summed by
+// the last-arriving item in fixed chunk order, attention splits merge in
+// split order, the argmax is an order-independent max over (value, ~index)
+// keys.  Nothing depends on the number of valid rows, so a row's logits are
+// the same whatever the verify window size (AMUSD tokens == AR tokens).
+#include <cuda.h>
+
+#include "common.cuh"
+#include "forward_tc.h"
+#include "internal.h"
+#include "tc_ptx.cuh"
+
+namespace amusd {
+namespace fw {
+
+using namespace amusd::tc;
+
+constexpr int kQ = 4;                  // item queue depth
+constexpr int kThreads = 320;
+constexpr int kWarpX = 1, kWarpMma0 = 2, kWarpEpi0 = 6;
+constexpr int kTbuf = 4;                 // TMEM accumulator buffers (MMA may run 3 items ahead of the epilogue)
+constexpr int kTmemCols = kTbuf * NACC * BN;  // 256
+constexpr int kAttnChunk = 128;        // positions per attention split (K/V chunk staged in smem)
+constexpr long long kWaitNs = 4ll * 1000 * 1000 * 1000;  // dependency waits trap after 4 s
+// Every schedule counter owns a 128-byte line (grab counter, exit counter, one
+// per phase, one per split-K tile): 148 CTAs poll and bump them concurrently.
+constexpr int kPad = kCounterInts;
+constexpr unsigned a_poll_ns = 100;
+
+// ------------------------------------------------------------ memory model
+AMUSD_DEV int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+AMUSD_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+// One round trip: release (this CTA's writes ordered before, via the preceding CTA barrier)
+// + acquire (the other contributors' writes visible after).
+AMUSD_DEV int atom_add_acq_rel(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+AMUSD_DEV void red_add_release(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+AMUSD_DEV void red_add_relaxed(int* p, int v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+AMUSD_DEV void wait_count(const int* p, int target) {
+  if (ld_acquire_gpu(p) >= target) return;
+  const long long t0 = globaltimer();
+  for (;;) {
+    __nanosleep(a_poll_ns);  // back off: many CTAs poll the same line
+    if (ld_acquire_gpu(p) >= target) return;
+    if (globaltimer() - t0 > kWaitNs) __trap();
+  }
+}
+
+// mbarrier wait with a wall-clock bound: a scheduling bug traps the kernel
+// (the host sees a launch error) instead of hanging the GPU.
+AMUSD_DEV void mbar_wait_t(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  if (ok) return;
+  const long long t0 = globaltimer();
+  for (int it = 0;; ++it) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if ((it & 255) == 255 && globaltimer() - t0 > kWaitNs) __trap();
+  }
+}
+
+// Optional per-item timeline (tools/fw_timeline.py): slot 0 item|cta<<20|phase<<32,
+// 1 grabbed, 2 weights issued, 3 X dependency met, 4 MMA done, 5 epilogue done.
+AMUSD_DEV void dbg_mark(const FwArgs& a, int item, int slot, long long v) {
+  if (a.dbg && item < a.dbg_items) a.dbg[(size_t)item * 8 + slot] = v;
+}
+
+// Bulk L2 prefetch of a contiguous weight range (no shared memory involved).
+AMUSD_DEV void prefetch_l2(const void* src, uint32_t bytes, uint64_t policy) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src), "r"(bytes), "l"(policy)
+               : "memory");
+}
+
+// Ring cursor: stage index + phase parity, advanced incrementally (no division).
+struct Ring {
+  int s = 0;
+  uint32_t ph = 0;
+  AMUSD_DEV void next(int S) {
+    if (++s == S) { s = 0; ph ^= 1u; }
+  }
+};
+
+// ------------------------------------------------------------ item layout
+// All schedule arithmetic comes from the kernel parameters (constant bank):
+// no role ever reads the schedule from global memory (the acquire polls
+// invalidate L1, which would turn every such read into an L2 round trip).
+struct Lay {
+  int A;       // attention items per layer (dynamic: rows x KV x splits)
+  int PL;      // items per layer
+  int total;   // items this launch
+  int rows, pos0;
+  int pre[5];  // first item of each layer phase relative to the layer's first item
+};
+
+AMUSD_DEV int nsplit_of(int p) { return p / kAttnChunk + 1; }
+
+AMUSD_DEV int kind_of(int p, int L) { return p == 0 ? kKEmbed : (p == 1 + 5 * L ? kKLm : (p - 1) % 5); }
+AMUSD_DEV int layer_of(int p) { return p == 0 ? 0 : (p - 1) / 5; }
+AMUSD_DEV int gemm_of(int kind) {
+  return kind == kKQkv ? kGQkv : kind == kKO ? kGO : kind == kKGu ? kGGu : kind == kKDown ? kGDown : kGLm;
+}
+AMUSD_DEV bool is_gemm(int kind) { return kind != kKAttn && kind != kKEmbed; }
+
+// item index -> (phase, index within the phase)
+AMUSD_DEV int2 locate(const FwArgs& a, const Lay& L, int i) {
+  if (i < KMAX) return make_int2(0, i);
+  int r = i - KMAX;
+  const int l = r / L.PL;
+  if (l >= a.L) return make_int2(1 + 5 * a.L, r - a.L * L.PL);
+  r -= l * L.PL;
+  int k = 4;
+  while (r < L.pre[k]) --k;
+  return make_int2(1 + 5 * l + k, r - L.pre[k]);
+}
+AMUSD_DEV int phase_first(const FwArgs& a, const Lay& L, int p) {
+  if (p == 0) return 0;
+  const int l = layer_of(p), k = p == 1 + 5 * a.L ? 0 : (p - 1) % 5;
+  return KMAX + l * L.PL + (p == 1 + 5 * a.L ? 0 : L.pre[k]);
+}
+AMUSD_DEV int phase_count(const FwArgs& a, const Lay& L, int p) {
+  const int kind = kind_of(p, a.L);
+  return kind == kKEmbed ? KMAX : kind == kKAttn ? L.A : a.g[gemm_of(kind)].nitems;
+}
+
+// A GEMM kind resolved for one layer.
+struct GemmRes {
+  const uint8_t* wt;
+  const __nv_bfloat16* gnext;
+  int epi, map, kb, kc, nchunks, nitems;
+};
+AMUSD_DEV GemmRes resolve(const FwArgs& a, int gk, int layer) {
+  const GemmKind& g = a.g[gk];
+  GemmRes r;
+  r.wt = g.wt + (size_t)layer * g.wt_stride;
+  r.gnext = g.gnext ? g.gnext + (size_t)layer * g.gnext_stride : nullptr;
+  r.epi = g.epi; r.map = g.map; r.kb = g.kb; r.kc = g.kc; r.nchunks = g.nchunks; r.nitems = g.nitems;
+  return r;
+}
+
+// ------------------------------------------------------------ epilogues
+struct EpiSmem {
+  float xchg[64 * BN];                // gate/up exchange
+  unsigned long long kx[4 * BN];      // argmax per lane-quarter
+  float sq[4 * BN];                   // residual sum-of-squares per lane-quarter
+  float inv[BN];
+  int flag;
+  int inv_phase;
+};
+
+// Final epilogue of one 128-row tile; thread holds tile row nl, v[r] for the
+// 16 token rows.  Activations written here are read by other CTAs of the same
+// launch: all loads/stores bypass L1 (.cg).
+AMUSD_DEV void tile_epilogue(const FwArgs& a, const GemmKind& ph, const __nv_bfloat16* gnext, int t, int nl,
+                             const float* v, int rows, EpiSmem* es, int q, int lane) {
+  const float* inv = es->inv;
+  if (ph.epi == kEpStoreScaled) {
+    const int n = t * BM + nl;
+#pragma unroll
+    for (int r = 0; r < BN; ++r)
+      if (r < rows) __stcg(ph.out + (size_t)r * ph.ldo + n, v[r] * inv[r]);
+  } else if (ph.epi == kEpResid) {
+    const int n = t * BM + nl;
+    const float gn = __bfloat162float(gnext[n]);
+#pragma unroll
+    for (int r = 0; r < BN; ++r) {
+      float hn = 0.f;
+      if (r < rows) {
+        hn = __ldcg(ph.out + (size_t)r * ph.ldo + n) + v[r];
+        __stcg(ph.out + (size_t)r * ph.ldo + n, hn);
+        ph.xnext[(size_t)r * ph.ldo + n] = __float2bfloat16(hn * gn);
+      }
+      const float s2 = warp_sum(hn * hn);
+      if (lane == 0) es->sq[q * BN + r] = s2;
+    }
+    named_bar(1, 128);
+    if (q == 0 && lane < BN) {  // fixed order over the 4 lane quarters
+      const float tot = es->sq[0 * BN + lane] + es->sq[1 * BN + lane] + es->sq[2 * BN + lane] + es->sq[3 * BN + lane];
+      __stcg(a.ssp + (size_t)lane * (a.d / BM) + t, lane < rows ? tot : 0.f);
+    }
+  } else if (ph.epi == kEpGateUp) {
+    // lanes 0..63: gate rows, 64..127: up rows of the same 64 features
+    if (nl >= 64) {
+#pragma unroll
+      for (int r = 0; r < BN; ++r) es->xchg[(nl - 64) * BN + r] = v[r];
+    }
+    named_bar(1, 128);
+    if (nl < 64) {
+      const int f = t * 64 + nl;
+#pragma unroll
+      for (int r = 0; r < BN; ++r) {
+        if (r < rows) {
+          const float g = v[r] * inv[r], u = es->xchg[nl * BN + r] * inv[r];
+          ph.out_b[(size_t)r * ph.ldo + f] = __float2bfloat16((g / (1.f + expf(-g))) * u);
+        }
+      }
+    }
+  } else {  // LM head: per-row argmax over the tile, merged by atomicMax (order independent)
+    const int n = t * BM + nl;
+    const bool valid_n = n < ph.N && !(a.exclude_eos && n == a.eos);
+#pragma unroll
+    for (int r = 0; r < BN; ++r) {
+      if (a.logits && n < ph.N && r < rows) a.logits[(size_t)r * ph.N + n] = v[r] * inv[r];
+      unsigned long long key = (valid_n && r < rows) ? argmax_key(v[r] * inv[r], n) : 0ull;
+      key = warp_max_u64(key);
+      if (lane == 0) es->kx[q * BN + r] = key;
+    }
+    named_bar(1, 128);
+    if (q == 0 && lane < BN && lane < rows) {
+      unsigned long long b = es->kx[lane];
+      for (int w = 1; w < 4; ++w) b = es->kx[w * BN + lane] > b ? es->kx[w * BN + lane] : b;
+      atomicMax(a.best + lane, b);
+    }
+  }
+}
+
+// ------------------------------------------------------------ SIMT items
+// Embedding of row r: h = E[tok], xa = bf16(h * g0), ssp per 128-wide tile.
+// Thread tid owns 16-byte vectors tid, tid+128, ...; a 128-wide tile is 16
+// consecutive vectors, reduced over 16 lanes (fixed shuffle tree).
+AMUSD_DEV void embed_item(const FwArgs& a, int r, int rows, int tid) {
+  const bool live = r < rows;
+  const uint4* src = (const uint4*)(a.embed + (size_t)(live ? a.ctl->tok[r] : 0) * a.d);
+  const uint4* gam = (const uint4*)a.norms;  // attention RMSNorm of layer 0
+  constexpr int kMaxVec = 8;  // d <= 8192
+  const int nv = a.d / 8;
+  uint4 x[kMaxVec], gv[kMaxVec];
+#pragma unroll
+  for (int k = 0; k < kMaxVec; ++k) {
+    const int q = tid + 128 * k;
+    if (q < nv) { x[k] = live ? src[q] : make_uint4(0, 0, 0, 0); gv[k] = gam[q]; }
+  }
+#pragma unroll
+  for (int k = 0; k < kMaxVec; ++k) {
+    const int q = tid + 128 * k;
+    if (q >= nv) break;
+    float f[8], g[8];
+    Elem<__nv_bfloat16>::unpack(x[k], f);
+    Elem<__nv_bfloat16>::unpack(gv[k], g);
+    float4* hp = (float4*)(a.h + (size_t)r * a.d + q * 8);
+    __stcg(hp, make_float4(f[0], f[1], f[2], f[3]));
+    __stcg(hp + 1, make_float4(f[4], f[5], f[6], f[7]));
+    uint4 o;
+    __nv_bfloat162 t0 = __floats2bfloat162_rn(f[0] * g[0], f[1] * g[1]), t1 = __floats2bfloat162_rn(f[2] * g[2], f[3] * g[3]);
+    __nv_bfloat162 t2 = __floats2bfloat162_rn(f[4] * g[4], f[5] * g[5]), t3 = __floats2bfloat162_rn(f[6] * g[6], f[7] * g[7]);
+    o.x = *(uint32_t*)&t0; o.y = *(uint32_t*)&t1; o.z = *(uint32_t*)&t2; o.w = *(uint32_t*)&t3;
+    *(uint4*)(a.xa + (size_t)r * a.d + q * 8) = o;
+    float ss = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ss += f[e] * f[e];
+    ss += __shfl_xor_sync(0xffffffffu, ss, 8);
+    ss += __shfl_xor_sync(0xffffffffu, ss, 4);
+    ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+    ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+    if ((tid & 15) == 0) __stcg(a.ssp + (size_t)r * (a.d / BM) + q / 16, ss);
+  }
+}
+
+// Attention scratch layout (epilogue warps only).
+template <int HD, int G>
+struct AttnSmem {
+  __nv_bfloat16 kb[kAttnChunk][HD];   // cached K rows of the chunk (bulk copy)
+  __nv_bfloat16 vb[kAttnChunk][HD];   // cached V rows of the chunk (bulk copy)
+  float qs[G][HD];                    // rotated queries of the group
+  float kn[KMAX][HD];                 // this step's rotated K rows (bf16-rounded) ...
+  float vn[KMAX][HD];                 // ... and V rows; red[4][G][HD] aliases kn/vn afterwards
+  float sc[G][kAttnChunk];            // scores -> probabilities
+  float stat[2][G];
+  float wred[4][G];
+  int last;
+  uint64_t bar;                       // K/V bulk-copy completion
+};
+
+// Issue the bulk copies of the cached K/V rows [lo, min(hi, pos0)) of head g
+// (they do not depend on this step): called before the QKV dependency wait.
+template <int HD, int G>
+AMUSD_DEV bool attn_prefetch(const FwArgs& a, AttnSmem<HD, G>* sm, int layer, int g, int lo, int hi, int pos0) {
+  const int tc = min(hi, pos0);
+  if (tc <= lo) return false;
+  const uint32_t bytes = (uint32_t)(tc - lo) * HD * 2;
+  const size_t off = ((size_t)g * a.S + lo) * HD * 2;
+  const char* kc = a.kcache + layer * a.kv_layer_bytes + off;
+  const char* vc = a.vcache + layer * a.kv_layer_bytes + off;
+  const uint32_t b = smem_u32(&sm->bar);
+  mbar_expect_tx(b, 2 * bytes);
+  const uint64_t pol = policy_evict_first();
+  bulk_load(smem_u32(&sm->kb[0][0]), kc, bytes, b, pol);
+  bulk_load(smem_u32(&sm->vb[0][0]), vc, bytes, b, pol);
+  return true;
+}
+
+// Decode/verify attention for (KV head g, window row r, position split): the
+// GROUP query heads of g together (K/V read once).  RoPE applied here; this
+// step's K/V rounded to bf16 exactly as a later step reads them from the
+// cache; the item owning position p appends row r's K/V; multi-split rows are
+// merged in split order by the last-arriving split.  Cached K/V come from
+// shared memory (staged before the dependency wait), so after the QKV phase
+// completes only the query rows cost a round trip.
+template <int HD, int G>
+AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint32_t bar_par, int layer, int g, int r,
+                         int split, int pos0, int tid) {
+  constexpr int DPL = HD / 32, NC = HD / 8;
+  const int wi = tid >> 5, lane = tid & 31;
+  float(*red)[G][HD] = (float(*)[G][HD])&sm->kn[0][0];
+  static_assert(4 * G <= 2 * KMAX, "red alias");
+  const int p = pos0 + r;
+  const int nsplit = nsplit_of(p);
+  const int lo = split * kAttnChunk, hi = min(p + 1, lo + kAttnChunk);
+  const int half = HD / 2, ncols = (a.H + 2 * a.KV) * HD;
+  const float* qkv = a.qkv;
+  for (int i = tid; i < G * half; i += 128) {
+    const int j = i / half, e = i - j * half;
+    const float* q = qkv + (size_t)r * ncols + (g * G + j) * HD;
+    const float c = a.cos[(size_t)p * half + e], s = a.sin[(size_t)p * half + e];
+    const float q0 = __ldcg(q + e), q1 = __ldcg(q + e + half);
+    sm->qs[j][e] = q0 * c - q1 * s;
+    sm->qs[j][e + half] = q1 * c + q0 * s;
+  }
+  const int jmax = hi > pos0 ? min(r, hi - 1 - pos0) : -1;
+  for (int i = tid; i < (jmax + 1) * half; i += 128) {
+    const int j = i / half, e = i - j * half;
+    const int pj = pos0 + j;
+    const float* kr = qkv + (size_t)j * ncols + (a.H + g) * HD;
+    const float c = a.cos[(size_t)pj * half + e], s = a.sin[(size_t)pj * half + e];
+    const float k0 = __ldcg(kr + e), k1 = __ldcg(kr + e + half);
+    sm->kn[j][e] = __bfloat162float(__float2bfloat16(k0 * c - k1 * s));
+    sm->kn[j][e + half] = __bfloat162float(__float2bfloat16(k1 * c + k0 * s));
+  }
+  for (int i = tid; i < (jmax + 1) * HD; i += 128) {
+    const int j = i / HD, e = i - j * HD;
+    sm->vn[j][e] = __bfloat162float(__float2bfloat16(__ldcg(qkv + (size_t)j * ncols + (a.H + a.KV + g) * HD + e)));
+  }
+  if (staged) mbar_wait_t(smem_u32(&sm->bar), bar_par);
+  named_bar(1, 128);
+  if (p >= lo && p < hi) {  // KV append for row r (pending-token scheme)
+    __nv_bfloat16* kc = (__nv_bfloat16*)(a.kcache + layer * a.kv_layer_bytes) + ((size_t)g * a.S + p) * HD;
+    __nv_bfloat16* vc = (__nv_bfloat16*)(a.vcache + layer * a.kv_layer_bytes) + ((size_t)g * a.S + p) * HD;
+    for (int e = tid; e < HD; e += 128) {
+      kc[e] = __float2bfloat16(sm->kn[r][e]);
+      vc[e] = __float2bfloat16(sm->vn[r][e]);
+    }
+  }
+  // ---- scores: thread per position (kAttnChunk == 128 == threads)
+  float mloc[G];
+#pragma unroll
+  for (int j = 0; j < G; ++j) mloc[j] = -INFINITY;
+  {
+    const int t = lo + tid;
+    if (t < hi) {
+      float dot[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j) dot[j] = 0.f;
+      if (t < pos0) {
+        const uint4* kt = (const uint4*)&sm->kb[t - lo][0];
+#pragma unroll 4
+        for (int cc = 0; cc < NC; ++cc) {
+          const int c = (cc + tid) % NC;  // rotated: a quarter-warp touches 8 distinct 16-byte bank groups
+          float f[8];
+          Elem<__nv_bfloat16>::unpack(kt[c], f);
+#pragma unroll
+          for (int j = 0; j < G; ++j) {
+            const float4 qa = *(const float4*)&sm->qs[j][8 * c], qb = *(const float4*)&sm->qs[j][8 * c + 4];
+            dot[j] = fmaf(f[0], qa.x, dot[j]); dot[j] = fmaf(f[1], qa.y, dot[j]);
+            dot[j] = fmaf(f[2], qa.z, dot[j]); dot[j] = fmaf(f[3], qa.w, dot[j]);
+            dot[j] = fmaf(f[4], qb.x, dot[j]); dot[j] = fmaf(f[5], qb.y, dot[j]);
+            dot[j] = fmaf(f[6], qb.z, dot[j]); dot[j] = fmaf(f[7], qb.w, dot[j]);
+          }
+        }
+      } else {
+        const float* kr = sm->kn[t - pos0];
+        for (int c = 0; c < HD; c += 4) {
+          const float4 kf = *(const float4*)&kr[c];
+#pragma unroll
+          for (int j = 0; j < G; ++j) {
+            const float4 qa = *(const float4*)&sm->qs[j][c];
+            dot[j] = fmaf(kf.x, qa.x, dot[j]); dot[j] = fmaf(kf.y, qa.y, dot[j]);
+            dot[j] = fmaf(kf.z, qa.z, dot[j]); dot[j] = fmaf(kf.w, qa.w, dot[j]);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const float sv = dot[j] * a.scale;
+        sm->sc[j][t - lo] = sv;
+        mloc[j] = sv;
+      }
+    }
+  }
+  // ---- softmax statistics per head (fixed reduction tree)
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    const float m = warp_max(mloc[j]);
+    if (lane == 0) sm->wred[wi][j] = m;
+  }
+  named_bar(1, 128);
+  float mj[G], lloc[G];
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    mj[j] = fmaxf(fmaxf(sm->wred[0][j], sm->wred[1][j]), fmaxf(sm->wred[2][j], sm->wred[3][j]));
+    lloc[j] = 0.f;
+  }
+  if (lo + tid < hi) {
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const float e = expf(sm->sc[j][tid] - mj[j]);
+      sm->sc[j][tid] = e;
+      lloc[j] = e;
+    }
+  }
+  named_bar(1, 128);  // wred reuse
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    const float l = warp_sum(lloc[j]);
+    if (lane == 0) sm->wred[wi][j] = l;
+  }
+  named_bar(1, 128);
+  if (tid < G) {
+    sm->stat[0][tid] = mj[tid];
+    sm->stat[1][tid] = (sm->wred[0][tid] + sm->wred[1][tid]) + (sm->wred[2][tid] + sm->wred[3][tid]);
+  }
+  // ---- unnormalised P.V from shared memory: warp w takes positions lo+w, lo+w+4, ...
+  float acc[G][DPL];
+#pragma unroll
+  for (int j = 0; j < G; ++j)
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) acc[j][e] = 0.f;
+  for (int t = lo + wi; t < hi; t += 4) {
+    float vv[DPL];
+    if (t < pos0) {
+      const __nv_bfloat16* vt = &sm->vb[t - lo][lane * DPL];
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) vv[e] = __bfloat162float(vt[e]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) vv[e] = sm->vn[t - pos0][lane * DPL + e];
+    }
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const float pj = sm->sc[j][t - lo];
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) acc[j][e] = fmaf(pj, vv[e], acc[j][e]);
+    }
+  }
+  named_bar(1, 128);  // everyone is done with kn/vn before red overwrites them
+#pragma unroll
+  for (int j = 0; j < G; ++j)
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) red[wi][j][lane * DPL + e] = acc[j][e];
+  named_bar(1, 128);
+  __nv_bfloat16* out = a.attn_b;
+  const int ldo = a.H * HD;
+  if (nsplit == 1) {
+    for (int i = tid; i < G * HD; i += 128) {
+      const int j = i / HD, e = i - j * HD;
+      const float o = red[0][j][e] + red[1][j][e] + red[2][j][e] + red[3][j][e];
+      out[(size_t)r * ldo + (g * G + j) * HD + e] = __float2bfloat16(o / sm->stat[1][j]);
+    }
+    return;
+  }
+  float* ws = a.attn_ws + (((size_t)g * KMAX + r) * a.max_splits + split) * G * (HD + 2);
+  for (int i = tid; i < G * HD; i += 128) {
+    const int j = i / HD, e = i - j * HD;
+    __stcg(ws + j * (HD + 2) + e, red[0][j][e] + red[1][j][e] + red[2][j][e] + red[3][j][e]);
+  }
+  if (tid < G) {
+    __stcg(ws + tid * (HD + 2) + HD, sm->stat[0][tid]);
+    __stcg(ws + tid * (HD + 2) + HD + 1, sm->stat[1][tid]);
+  }
+  named_bar(1, 128);
+  if (tid == 0) {
+    int* cnt = a.attn_cnt + (g * KMAX + r) * kPad;
+    const int old = atom_add_acq_rel(cnt, 1);
+    sm->last = (old == nsplit - 1);
+    if (sm->last) *cnt = 0;
+  }
+  named_bar(1, 128);
+  if (!sm->last) return;
+  const float* base = a.attn_ws + ((size_t)g * KMAX + r) * a.max_splits * G * (HD + 2);
+  for (int i = tid; i < G * HD; i += 128) {
+    const int j = i / HD, e = i - j * HD;
+    float M = -INFINITY;
+    for (int s2 = 0; s2 < nsplit; ++s2) M = fmaxf(M, __ldcg(base + ((size_t)s2 * G + j) * (HD + 2) + HD));
+    float Ls = 0.f, O = 0.f;
+    for (int s2 = 0; s2 < nsplit; ++s2) {
+      const float* w = base + ((size_t)s2 * G + j) * (HD + 2);
+      const float f = expf(__ldcg(w + HD) - M);
+      Ls += __ldcg(w + HD + 1) * f;
+      O += __ldcg(w + e) * f;
+    }
+    out[(size_t)r * ldo + (g * G + j) * HD + e] = __float2bfloat16(O / Ls);
+  }
+}
+
+// ------------------------------------------------------------ the kernel
+template <int HD, int G>
+constexpr int attn_scratch_bytes() {
+  return ((int)sizeof(AttnSmem<HD, G>) + 127) & ~127;
+}
+constexpr int epi_bytes() { return ((int)sizeof(EpiSmem) + 127) & ~127; }
+
+template <int HD, int G, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+    k_forward(const __grid_constant__ CUtensorMap m_xa, const __grid_constant__ CUtensorMap m_attn,
+              const __grid_constant__ CUtensorMap m_act, const __grid_constant__ FwArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int S = a.stages;
+  uint8_t* sW = smem;
+  uint8_t* sX = smem + S * kWBytes;
+  uint8_t* scratch = sX + S * kXBytes;  // attention scratch / epilogue exchange (epilogue warps only)
+  constexpr int kAttnBytes = attn_scratch_bytes<HD, G>();
+  constexpr int kScratch = kAttnBytes + epi_bytes();
+  uint64_t* bars = (uint64_t*)(scratch + kScratch);
+  uint64_t* wfull = bars;
+  uint64_t* xfull = bars + S;
+  uint64_t* empty = bars + 2 * S;
+  uint64_t* tfull = bars + 3 * S;
+  uint64_t* tempty = tfull + kTbuf;
+  uint64_t* qfull = tempty + kTbuf;
+  uint64_t* qempty = qfull + kQ;
+  int2* queue = (int2*)(qempty + kQ);
+  uint32_t* tmem_slot = (uint32_t*)(queue + kQ);
+  int* s_lay = (int*)(tmem_slot + 1);  // A, rows, pos0, active
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    const StepCtl* c = a.ctl;
+    const int active = c->active;
+    const int rows = active ? c->rows : 0, pos0 = c->pos0;
+    int A = 0;
+    for (int r = 0; r < rows; ++r) A += a.KV * nsplit_of(pos0 + r);
+    s_lay[0] = A;
+    s_lay[1] = rows;
+    s_lay[2] = pos0;
+    s_lay[3] = active;
+    for (int s = 0; s < S; ++s) {
+      mbar_init(smem_u32(&wfull[s]), 1);
+      mbar_init(smem_u32(&xfull[s]), 1);
+      mbar_init(smem_u32(&empty[s]), NACC);
+    }
+    for (int i = 0; i < kTbuf; ++i) { mbar_init(smem_u32(&tfull[i]), NACC); mbar_init(smem_u32(&tempty[i]), 128); }
+    for (int i = 0; i < kQ; ++i) { mbar_init(smem_u32(&qfull[i]), 1); mbar_init(smem_u32(&qempty[i]), 1 + NACC + 1); }
+    mbar_init(smem_u32(&((AttnSmem<HD, G>*)scratch)->bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (!s_lay[3]) return;  // inactive step: nothing grabbed, nothing to reset
+  Lay L;
+  L.A = s_lay[0]; L.rows = s_lay[1]; L.pos0 = s_lay[2];
+  L.pre[0] = 0;
+  L.pre[1] = a.g[kGQkv].nitems;
+  L.pre[2] = L.pre[1] + L.A;
+  L.pre[3] = L.pre[2] + a.g[kGO].nitems;
+  L.pre[4] = L.pre[3] + a.g[kGGu].nitems;
+  L.PL = L.pre[4] + a.g[kGDown].nitems;
+  L.total = KMAX + a.L * L.PL + a.g[kGLm].nitems;
+  if (warp == kWarpMma0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  int* done = a.sched + 2 * kPad;  // done count of phase p at done[p * kPad]
+
+  if (warp == 0) {
+    // ===== scheduler + weight producer =====
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();  // weights stream once
+      int n = 0;
+      long long gu = 0;
+      Ring rg, rl;  // rg: stage being filled; rl: stage `inflight` units behind (outstanding cap)
+      // Optional L2 prefetch stream (AMUSD_FW_L2_MB): the grabber of item i prefetches item i + ahead.
+      const uint64_t pol_keep = policy_evict_last();
+      const int ahead = a.prefetch_items;
+      const int inflight = a.inflight > 0 ? min(a.inflight, S) : S;
+      auto prefetch_item = [&](int k) {
+        if (k >= L.total) return;
+        const int2 pj = locate(a, L, k);
+        const int kind = kind_of(pj.x, a.L);
+        if (!is_gemm(kind)) return;
+        const GemmRes g = resolve(a, gemm_of(kind), layer_of(pj.x));
+        const int t = pj.y / g.nchunks, c = pj.y - t * g.nchunks;
+        prefetch_l2(g.wt + ((size_t)t * g.kb + (size_t)c * g.kc) * kWBytes, (uint32_t)g.kc * kWBytes, pol_keep);
+      };
+      if (ahead > 0)  // the first `ahead` items have no earlier grabber: spread them over the CTAs
+        for (int k = blockIdx.x; k < ahead; k += gridDim.x) prefetch_item(k);
+      int i_next = atomicAdd(a.sched, 1);  // grab counter: sched[0]; exit counter: sched[kPad]
+      for (;;) {
+        // the grab of the following item is in flight while this one streams
+        const int i = i_next;
+        if (i < L.total) i_next = atomicAdd(a.sched, 1);
+        if (ahead > 0 && i < L.total) prefetch_item(i + ahead);
+        const int slot = n % kQ;
+        mbar_wait_t(smem_u32(&qempty[slot]), ((n / kQ) & 1) ^ 1);
+        if (i >= L.total) {
+          queue[slot] = make_int2(-1, 0);
+          mbar_arrive(smem_u32(&qfull[slot]));
+          break;
+        }
+        const int2 pj = locate(a, L, i);
+        dbg_mark(a, i, 0, (long long)i | ((long long)blockIdx.x << 20) | ((long long)pj.x << 32));
+        dbg_mark(a, i, 1, globaltimer());
+        queue[slot] = pj;
+        mbar_arrive(smem_u32(&qfull[slot]));
+        ++n;
+        const int kind = kind_of(pj.x, a.L);
+        if (is_gemm(kind)) {
+          const GemmRes g = resolve(a, gemm_of(kind), layer_of(pj.x));
+          const int t = pj.y / g.nchunks, c = pj.y - t * g.nchunks;
+          const uint8_t* src = g.wt + ((size_t)t * g.kb + (size_t)c * g.kc) * kWBytes;
+          for (int u = 0; u < g.kc; ++u, ++gu, rg.next(S)) {
+            const int s = rg.s;
+            mbar_wait_t(smem_u32(&empty[s]), rg.ph ^ 1u);
+            // Optional outstanding-load cap (AMUSD_FW_INFLIGHT): at most `inflight` unlanded units.
+            if (inflight < S && gu >= inflight) {
+              mbar_wait_t(smem_u32(&wfull[rl.s]), rl.ph);
+              rl.next(S);
+            }
+            if (a.debug & 8) {  // perf isolation: no weight traffic
+              mbar_arrive(smem_u32(&wfull[s]));
+              continue;
+            }
+            mbar_expect_tx(smem_u32(&wfull[s]), kWBytes);
+            bulk_load(smem_u32(sW + s * kWBytes), src + (size_t)u * kWBytes, kWBytes, smem_u32(&wfull[s]), pol_w);
+          }
+          dbg_mark(a, i, 2, globaltimer());
+        }
+      }
+    }
+  } else if (warp == kWarpX) {
+    // ===== activation loader: dependency wait, then X tiles by TMA =====
+    if (lane == 0) {
+      const uint64_t pol_x = policy_evict_last();  // X is re-read by every CTA of the phase
+      int n = 0, dep_ok = -1;
+      Ring rg;
+      for (;;) {
+        const int slot = n % kQ;
+        mbar_wait_t(smem_u32(&qfull[slot]), (n / kQ) & 1);
+        const int2 it = queue[slot];
+        mbar_arrive(smem_u32(&qempty[slot]));
+        ++n;
+        if (it.x < 0) break;
+        const int kind = kind_of(it.x, a.L);
+        if (!is_gemm(kind)) continue;
+        const int dep = it.x - 1;
+        if (dep > dep_ok && !(a.debug & 2)) {  // debug bit 1: ignore GEMM dependencies (timing only)
+          wait_count(done + dep * kPad, phase_count(a, L, dep));
+          fence_proxy_async();
+          dep_ok = dep;
+        }
+        if (a.dbg) dbg_mark(a, phase_first(a, L, it.x) + it.y, 3, globaltimer());
+        const GemmKind& g = a.g[gemm_of(kind)];
+        const CUtensorMap* map = g.map == 0 ? &m_xa : (g.map == 1 ? &m_attn : &m_act);
+        const int c = it.y % g.nchunks, kc = g.kc;
+        for (int u = 0; u < kc; ++u, rg.next(S)) {
+          const int s = rg.s;
+          mbar_wait_t(smem_u32(&empty[s]), rg.ph ^ 1u);
+          if (a.debug & 4) {  // perf isolation: no activation traffic
+            mbar_arrive(smem_u32(&xfull[s]));
+            continue;
+          }
+          mbar_expect_tx(smem_u32(&xfull[s]), kXBytes);
+          tma_load_2d(smem_u32(sX + s * kXBytes), map, (c * kc + u) * BK, 0, smem_u32(&xfull[s]), pol_x);
+        }
+      }
+    }
+  } else if (warp < kWarpEpi0) {
+    // ===== MMA issuers: warp w issues K-slice kk of every unit =====
+    if (lane == 0) {
+      const int kk = warp - kWarpMma0;
+      int n = 0, seg = 0;
+      Ring rg;
+      for (;;) {
+        const int slot = n % kQ;
+        mbar_wait_t(smem_u32(&qfull[slot]), (n / kQ) & 1);
+        const int2 it = queue[slot];
+        mbar_arrive(smem_u32(&qempty[slot]));
+        ++n;
+        if (it.x < 0) break;
+        const int kind = kind_of(it.x, a.L);
+        if (!is_gemm(kind)) continue;
+        const int kc = a.g[gemm_of(kind)].kc;
+        const int b = seg % kTbuf;
+        mbar_wait_t(smem_u32(&tempty[b]), ((seg / kTbuf) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)((b * NACC + kk) * BN);
+        for (int u = 0; u < kc; ++u, rg.next(S)) {
+          const int s = rg.s;
+          const uint32_t par = rg.ph;
+          mbar_wait_t(smem_u32(&wfull[s]), par);
+          mbar_wait_t(smem_u32(&xfull[s]), par);
+          tc_fence_after();
+          if (a.debug & 1) {  // perf isolation: consume the stage without an MMA
+            mbar_arrive(smem_u32(&empty[s]));
+            continue;
+          }
+          umma(d, umma_desc(smem_u32(sW + s * kWBytes) + kk * 32), umma_desc(smem_u32(sX + s * kXBytes) + kk * 32),
+               u > 0 ? 1u : 0u);
+          umma_commit(smem_u32(&empty[s]));
+        }
+        if (a.debug & 1) mbar_arrive(smem_u32(&tfull[b]));
+        else umma_commit(smem_u32(&tfull[b]));
+        ++seg;
+      }
+    }
+  } else {
+    // ===== epilogue + SIMT items (128 threads) =====
+    const int tid = threadIdx.x - 32 * kWarpEpi0;
+    const int q = warp & 3;        // TMEM lane quarter this warp may access
+    const int nl = q * 32 + lane;  // tile row held by this thread
+    EpiSmem* es = (EpiSmem*)(scratch + kAttnBytes);  // never aliased by the attention scratch
+    if (tid == 0) es->inv_phase = -1;
+    int n = 0, seg = 0, dep_ok = -1;
+    uint32_t attn_par = 0;
+    for (;;) {
+      const int slot = n % kQ;
+      mbar_wait_t(smem_u32(&qfull[slot]), (n / kQ) & 1);
+      const int2 it = queue[slot];
+      named_bar(1, 128);
+      if (tid == 0) mbar_arrive(smem_u32(&qempty[slot]));
+      ++n;
+      if (it.x < 0) break;
+      const int p = it.x, j = it.y;
+      const int kind = kind_of(p, a.L), layer = layer_of(p);
+      bool wrote = true, lm_last_check = false;
+      if (is_gemm(kind)) {
+        const GemmKind& g = a.g[gemm_of(kind)];
+        const int b = seg % kTbuf;
+        mbar_wait_t(smem_u32(&tfull[b]), (seg / kTbuf) & 1);
+        tc_fence_after();
+        if (a.dbg && tid == 0) dbg_mark(a, phase_first(a, L, p) + j, 4, globaltimer());
+        float v[BN];
+        {
+          const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * NACC * BN);
+          float w[BN];
+          tmem_ld16(base, v);
+#pragma unroll
+          for (int c = 1; c < NACC; ++c) {  // fixed chain order
+            tmem_ld16(base + c * BN, w);
+#pragma unroll
+            for (int r = 0; r < BN; ++r) v[r] += w[r];
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(smem_u32(&tempty[b]));
+        ++seg;
+        const int epi = g.epi, nchunks = g.nchunks;
+        // RMSNorm scale of the phase's input rows (once per phase per CTA)
+        const bool need_inv = epi == kEpStoreScaled || epi == kEpGateUp || epi == kEpArgmax;
+        if (need_inv && es->inv_phase != p) {
+          // 8 threads per row, each a strided slice of the row's tile sums; fixed shuffle tree
+          const int nt = a.d / BM, rr = tid >> 3, part = tid & 7;
+          float tot = 0.f;
+          for (int k = part; k < nt; k += 8) tot += __ldcg(a.ssp + (size_t)rr * nt + k);
+          tot += __shfl_xor_sync(0xffffffffu, tot, 1);
+          tot += __shfl_xor_sync(0xffffffffu, tot, 2);
+          tot += __shfl_xor_sync(0xffffffffu, tot, 4);
+          named_bar(1, 128);
+          if (part == 0) es->inv[rr] = rsqrtf(tot / (float)a.d + a.eps);
+          named_bar(1, 128);
+          if (tid == 0) es->inv_phase = p;
+        }
+        const int t = j / nchunks;
+        bool final = true;
+        float acc[BN];
+        if (nchunks > 1) {
+          // Split-K in exact int64 fixed point (2^-32): the red.adds commute, so the merged
+          // tile is bit-identical whatever the chunks' arrival order (deterministic, batch
+          // invariant) and no partial ever needs a merge round trip.  Layout [tile][row][128].
+          unsigned long long* acc64 = (unsigned long long*)a.ws + (size_t)t * BN * BM + nl;
+#pragma unroll
+          for (int r = 0; r < BN; ++r) {
+            const long long fx = __float2ll_rn(v[r] * 4294967296.0f);
+            asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(acc64 + r * BM), "l"(fx) : "memory");
+          }
+          named_bar(1, 128);
+          // The tile's last chunk (grabbed after its other chunks) merges; the others publish
+          // with a fire-and-forget release and move on -- no round trip in their epilogue.
+          final = (j - t * nchunks) == nchunks - 1;
+          if (!final) {
+            if (tid == 0) red_add_release(a.tile_cnt + t * kPad, 1);
+          } else {
+            if (tid == 0) {
+              wait_count(a.tile_cnt + t * kPad, nchunks - 1);
+              a.tile_cnt[t * kPad] = 0;  // re-arm for the next phase / launch
+            }
+            named_bar(1, 128);
+            long long s64[BN];
+#pragma unroll
+            for (int r = 0; r < BN; ++r) s64[r] = (long long)__ldcg(acc64 + r * BM);
+#pragma unroll
+            for (int r = 0; r < BN; ++r) {
+              acc[r] = (float)((double)s64[r] * (1.0 / 4294967296.0));
+              __stcg(acc64 + r * BM, 0ull);  // re-arm the accumulator (next use is a later phase)
+            }
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < BN; ++r) acc[r] = v[r];
+        }
+        if (final) {
+          const __nv_bfloat16* gnext = g.gnext ? g.gnext + (size_t)layer * g.gnext_stride : nullptr;
+          tile_epilogue(a, g, gnext, t, nl, acc, L.rows, es, q, lane);
+        }
+        wrote = final;
+        lm_last_check = epi == kEpArgmax;
+      } else if (kind == kKEmbed) {
+        embed_item(a, j, L.rows, tid);
+      } else {  // attention
+        int r = 0, rem = j;
+        for (;;) {
+          const int cnt = a.KV * nsplit_of(L.pos0 + r);
+          if (rem < cnt) break;
+          rem -= cnt;
+          ++r;
+        }
+        const int gh = rem % a.KV, split = rem / a.KV;
+        const int lo = split * kAttnChunk, hi = min(L.pos0 + r + 1, lo + kAttnChunk);
+        AttnSmem<HD, G>* asm_ = (AttnSmem<HD, G>*)scratch;
+        // the cached K/V rows do not depend on this step: stage them before the wait
+        bool staged = false;
+        if (tid == 0) {
+          staged = attn_prefetch<HD, G>(a, asm_, layer, gh, lo, hi, L.pos0);
+          asm_->last = staged;
+        }
+        const int dep = p - 1;
+        if (dep > dep_ok) {
+          if (tid == 0) wait_count(done + dep * kPad, phase_count(a, L, dep));
+          dep_ok = dep;
+        }
+        named_bar(1, 128);
+        staged = asm_->last;
+        attn_item<HD, G>(a, asm_, staged, attn_par, layer, gh, r, split, L.pos0, tid);
+        if (staged) attn_par ^= 1u;
+      }
+      // publish: this item's writes are visible (generic and async proxy) before the count
+      // (CTA barrier, then one release by thread 0: the cooperative-groups grid-sync pattern).
+      if (wrote) fence_proxy_async();
+      named_bar(1, 128);
+      if (tid == 0) {
+        if (a.dbg) dbg_mark(a, phase_first(a, L, p) + j, 5, globaltimer());
+        if (lm_last_check) {
+          const int old = atom_add_acq_rel(done + p * kPad, 1);
+          if (old == a.g[kGLm].nitems - 1) {  // last LM-head item: final argmax per row
+            for (int r = 0; r < L.rows; ++r) {
+              const unsigned long long k = atomicExch(a.best + r, 0ull);
+              a.ctl->preds[r] = argmax_key_index(k);
+            }
+          }
+        } else if (wrote) {
+          red_add_release(done + p * kPad, 1);
+        } else {
+          // non-final split-K item: its partial was released by the tile count; the consumers'
+          // acquire of the phase count reaches the final items' releases through the RMW chain
+          red_add_relaxed(done + p * kPad, 1);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == kWarpMma0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int old = atomicAdd(a.sched + kPad, 1);
+    if (old == (int)gridDim.x - 1) {  // last CTA out: re-arm the schedule for the next launch
+      a.sched[0] = 0;
+      a.sched[kPad] = 0;
+      for (int i = 0; i < num_phases(a.L); ++i) done[i * kPad] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// ------------------------------------------------------------ host side
+int attn_items_max(int KV, int S) { return KV * KMAX * attn_splits(S); }
+int attn_splits(int S) { return (S + kAttnChunk - 1) / kAttnChunk; }
+
+static int pick_kc(int kb, int target) {
+  int best = 1;
+  for (int k = 1; k <= kb; ++k)
+    if (kb % k == 0 && k <= target) best = k;
+  return best;
+}
+
+void build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_floats, int* max_tiles) {
+  const int ncols = (m.H + 2 * m.KV) * m.hd, hh = m.H * m.hd;
+  const long long b_qkv = (long long)ncols * m.d * 2, b_o = (long long)m.d * hh * 2, b_gu = 2ll * m.ffn * m.d * 2;
+  size_t wsf = 0;
+  int mt = 0;
+  auto kind = [&](int epi, int map, int ntiles, int K, int N, int ldo, const uint8_t* wt, long long stride) {
+    GemmKind g{};
+    g.epi = epi; g.map = map; g.ntiles = ntiles; g.kb = K / BK;
+    g.kc = pick_kc(g.kb, units_per_item);
+    g.nchunks = g.kb / g.kc;
+    g.nitems = ntiles * g.nchunks;
+    g.N = N; g.ldo = ldo; g.wt = wt; g.wt_stride = stride;
+    if (g.nchunks > 1) wsf = std::max(wsf, (size_t)g.ntiles * BM * BN * 2);  // int64 accumulator tiles
+    mt = std::max(mt, ntiles);
+    return g;
+  };
+  const uint8_t* w0 = m.wt_layer0;
+  a->g[kGQkv] = kind(kEpStoreScaled, 0, ncols / BM, m.d, ncols, ncols, w0, m.wt_layer_bytes);
+  a->g[kGQkv].out = m.qkv;
+  a->g[kGO] = kind(kEpResid, 1, m.d / BM, hh, m.d, m.d, w0 + b_qkv, m.wt_layer_bytes);
+  a->g[kGO].out = m.h; a->g[kGO].xnext = m.xa;
+  a->g[kGO].gnext = m.norms + m.d;          // mlp RMSNorm of layer l at 2l+1
+  a->g[kGO].gnext_stride = 2 * m.d;
+  a->g[kGGu] = kind(kEpGateUp, 0, m.ffn / 64, m.d, m.ffn, m.ffn, w0 + b_qkv + b_o, m.wt_layer_bytes);
+  a->g[kGGu].out_b = m.act_b;
+  a->g[kGDown] = kind(kEpResid, 2, m.d / BM, m.ffn, m.d, m.d, w0 + b_qkv + b_o + b_gu, m.wt_layer_bytes);
+  a->g[kGDown].out = m.h; a->g[kGDown].xnext = m.xa;
+  a->g[kGDown].gnext = m.norms + 2 * m.d;   // attention RMSNorm of layer l+1 at 2l+2 (final norm at 2L)
+  a->g[kGDown].gnext_stride = 2 * m.d;
+  a->g[kGLm] = kind(kEpArgmax, 0, m.vocab / BM, m.d, m.vocab, m.vocab, m.wt_lm, 0);
+  a->L = m.L;
+  a->attn_max = attn_items_max(m.KV, m.S);
+  *ws_floats = wsf;
+  *max_tiles = mt;
+}
+
+template <int HD, int G>
+static constexpr int scratch_bytes() {
+  return attn_scratch_bytes<HD, G>() + epi_bytes();
+}
+
+int forward_smem_bytes(int stages, int hd, int group) {
+  int sc = 0;
+#define AMUSD_SC(HD_, G_) \
+  if (hd == HD_ && group == G_) sc = scratch_bytes<HD_, G_>();
+  AMUSD_SC(64, 2) AMUSD_SC(64, 4) AMUSD_SC(64, 8) AMUSD_SC(128, 2) AMUSD_SC(128, 4) AMUSD_SC(128, 8)
+#undef AMUSD_SC
+  if (!sc) return 0;
+  const int ctl = (3 * stages + 2 * kTbuf + 2 * kQ) * 8 + kQ * 8 + 4 + 5 * 4;
+  return 1024 + stages * (kWBytes + kXBytes) + sc + ((ctl + 127) & ~127);
+}
+
+template <int HD, int G, int MINB>
+static cudaError_t launch_m(const FwArgs& a, const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& m2,
+                            int grid, int stages, cudaStream_t st) {
+  const int smem = forward_smem_bytes(stages, HD, G);
+  static int attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_forward<HD, G, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  FwArgs b = a;
+  b.stages = stages;
+  k_forward<HD, G, MINB><<<grid, kThreads, smem, st>>>(m0, m1, m2, b);
+  return cudaGetLastError();
+}
+
+// Rings small enough for two CTAs per SM (co-located draft + verify forwards)
+// take the register-capped instance so that two CTAs fit the register file too.
+template <int HD, int G>
+static cudaError_t launch_t(const FwArgs& a, const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& m2,
+                            int grid, int stages, cudaStream_t st) {
+  if (forward_smem_bytes(stages, HD, G) <= 232448 / 2 - 1024)
+    return launch_m<HD, G, 2>(a, m0, m1, m2, grid, stages, st);
+  return launch_m<HD, G, 1>(a, m0, m1, m2, grid, stages, st);
+}
+
+cudaError_t launch_forward(const FwArgs& a, const CUtensorMap& m_xa, const CUtensorMap& m_attn,
+                           const CUtensorMap& m_act, int grid, int stages, cudaStream_t st) {
+  const int G = a.H / a.KV;
+#define AMUSD_FW(HD_, G_) \
+  if (a.hd == HD_ && G == G_) return launch_t<HD_, G_>(a, m_xa, m_attn, m_act, grid, stages, st);
+  AMUSD_FW(64, 2) AMUSD_FW(64, 4) AMUSD_FW(64, 8) AMUSD_FW(128, 2) AMUSD_FW(128, 4) AMUSD_FW(128, 8)
+#undef AMUSD_FW
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace fw
+}  // namespace amusd

@@ -1,0 +1,99 @@
+// forward_tc.h -- persistent tcgen05 decoder forward: ONE launch per model
+// forward (draft next_token+advance, models.py:120-131; verify
+// verify_tokens+advance, models.py:151-169), replacing 1 + 5L + 2 kernels.
+#pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace amusd {
+namespace fw {
+
+// Phase kinds.  Phase p: 0 = embedding; 1 + 5l + k = layer l, k in
+// {QKV, ATTN, O, GU, DOWN}; 1 + 5L = LM head.  Every phase depends on p-1.
+enum { kKQkv = 0, kKAttn = 1, kKO = 2, kKGu = 3, kKDown = 4, kKEmbed = 5, kKLm = 6 };
+// GEMM epilogues
+enum { kEpStoreScaled = 0, kEpResid = 1, kEpGateUp = 2, kEpArgmax = 3 };
+// GEMM kinds in FwArgs::g[]
+enum { kGQkv = 0, kGO = 1, kGGu = 2, kGDown = 3, kGLm = 4, kNumGemm = 5 };
+
+// One GEMM of the layer (identical shape in every layer; per-layer pointers
+// are base + layer * stride).  Lives in the kernel parameters (constant
+// bank): the persistent kernel never reads its schedule from global memory.
+struct GemmKind {
+  const uint8_t* wt;            // tile-contiguous SW128 weights (16 KB per unit), layer 0
+  long long wt_stride;          // bytes between layers
+  float* out;                   // StoreScaled / Resid output (fp32)
+  __nv_bfloat16* out_b;         // GateUp output (bf16)
+  __nv_bfloat16* xnext;         // Resid: next GEMM input bf16(h * gnext)
+  const __nv_bfloat16* gnext;   // Resid: next RMSNorm weight, layer 0
+  int gnext_stride;             // elements between layers
+  int epi, map;                 // epilogue, X tensor map (0 xa [16][d], 1 attn [16][H*hd], 2 act [16][ffn])
+  int ntiles, kb, kc, nchunks, nitems;  // 128-row tiles, 64-wide K units per tile, units per item, items per tile
+  int N, ldo;
+};
+
+struct FwArgs {
+  GemmKind g[kNumGemm];
+  int L;                        // layers
+  int attn_max;                 // attention items per layer for 16 rows at max_seq (sizing only)
+  StepCtl* ctl;
+  int* sched;                   // 128-byte lines: [0] next item, [1] exit count, [2 + p] done count of phase p (self-resetting)
+  // model
+  const __nv_bfloat16* embed;
+  const __nv_bfloat16* norms;   // packed RMSNorm weights [2L+1][d]: attn(l) at 2l, mlp(l) at 2l+1, final at 2L
+  float* h;                     // [16][d] residual stream
+  __nv_bfloat16* xa;            // [16][d] bf16(h * g) input of QKV / gate-up / LM head
+  float* ssp;                   // [16][d/128] per-tile sum of squares of h
+  float* qkv;                   // [16][(H+2KV)hd]
+  __nv_bfloat16* attn_b;        // [16][H hd]
+  char* kcache;                 // [L][KV][S][hd] bf16
+  char* vcache;
+  long long kv_layer_bytes;
+  float* ws;                    // split-K partials [ntiles*nchunks][128][16]
+  int* tile_cnt;                // split-K arrival counters, one 128-byte line per tile (self-resetting)
+  float* attn_ws;               // attention split partials
+  int* attn_cnt;
+  const float* cos;
+  const float* sin;
+  unsigned long long* best;     // [16] argmax keys (self-resetting)
+  float* logits;                // optional [16][V]
+  int d, H, KV, hd, S, max_splits, vocab, eos, exclude_eos;
+  float scale, eps;
+  int stages;
+  int prefetch_items;           // L2 prefetch distance in work items (0 = off)
+  int inflight;                 // max unlanded weight units per CTA (0 = ring depth)
+  int debug;                    // perf-isolation bits (AMUSD_FW_DEBUG), 0 in production
+  long long* dbg;               // optional per-item timeline [item][8] (perf analysis), null in production
+  int dbg_items;
+};
+
+__host__ __device__ inline int num_phases(int L) { return 2 + 5 * L; }
+constexpr int kCounterInts = 32;  // ints per schedule counter (one 128-byte line)
+int attn_items_max(int KV, int S);
+int attn_splits(int S);  // position splits of the persistent forward's attention (128-position chunks)
+
+// Host: fill the GEMM kinds of a model (tiled weights laid out per layer as
+// [qkv | o | gate-up | down], LM head after the last layer).
+struct ModelView {
+  int d, H, KV, hd, ffn, vocab, L, S;
+  const uint8_t* wt_layer0;     // tiled weights of layer 0 (qkv first)
+  long long wt_layer_bytes;
+  const uint8_t* wt_lm;
+  const __nv_bfloat16* norms;   // packed [2L+1][d]
+  float* h;
+  float* qkv;
+  __nv_bfloat16* xa;
+  __nv_bfloat16* act_b;
+};
+void build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_floats, int* max_tiles);
+
+cudaError_t launch_forward(const FwArgs& a, const CUtensorMap& m_xa, const CUtensorMap& m_attn,
+                           const CUtensorMap& m_act, int grid, int stages, cudaStream_t st);
+int forward_smem_bytes(int stages, int hd, int group);
+
+}  // namespace fw
+}  // namespace amusd

@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "gemm_tc.h"
 #include "internal.h"
+#include "tc_ptx.cuh"
 
 namespace amusd {
 namespace tc {
@@ -31,123 +32,10 @@ namespace tc {
 // K-slices of each stage are therefore issued by 4 different warps, each into
 // its own TMEM accumulator chain (summed in fixed order by the epilogue:
 // deterministic and batch-invariant).
-constexpr int BM = 128;           // weight rows per tile (gate/up: 64 gate + 64 up)
-constexpr int BN = 16;            // token rows
-constexpr int BK = 64;            // K per stage (one 128-byte swizzle atom)
-constexpr int NACC = BK / 16;     // MMA issuer warps / accumulator chains
 constexpr int STAGES = 5;         // ~96 KB smem: two CTAs per SM (PDL prefetch overlap)
 constexpr int kThreads = 32 * (1 + NACC + 4);  // w0 TMA, w1..w4 MMA issuers, w5..w8 epilogue
-constexpr int kWBytes = BM * BK * 2;  // 16 KB weight unit (one bulk copy)
-constexpr int kXBytes = BN * BK * 2;  // 2 KB token tile (TMA)
 constexpr int kTmemCols = 2 * NACC * BN;  // double-buffered: 128 columns
 constexpr int smem_bytes() { return STAGES * (kWBytes + kXBytes) + 1024 + 4096 + 512; }
-
-// ---------------------------------------------------------------- PTX
-AMUSD_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-AMUSD_DEV void mbar_init(uint32_t a, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
-}
-AMUSD_DEV void mbar_expect_tx(uint32_t a, int bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
-}
-AMUSD_DEV void mbar_arrive(uint32_t a) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
-}
-// Bounded wait: a protocol bug must surface as a trapped kernel, never as a
-// hung GPU (try_wait suspends up to the hardware time limit per probe).
-AMUSD_DEV void mbar_wait(uint32_t a, uint32_t parity) {
-  for (long long it = 0;; ++it) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-    if (ok) return;
-    if (it > (1ll << 26)) __trap();
-  }
-}
-AMUSD_DEV void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
-      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(mbar), "l"(policy)
-      : "memory");
-}
-// 1-D bulk copy global -> shared (contiguous bytes), completion on an mbarrier.
-AMUSD_DEV void bulk_load(uint32_t dst, const void* src, int bytes, uint32_t mbar, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(mbar), "l"(policy)
-      : "memory");
-}
-AMUSD_DEV uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-AMUSD_DEV uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-AMUSD_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-AMUSD_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-
-// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, SBO = 1024 B (8 rows x 128 B).
-AMUSD_DEV uint64_t umma_desc(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
-  d |= (uint64_t)1 << 16;                          // LBO (unused for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;                // SBO
-  d |= (uint64_t)1 << 46;                          // descriptor version (Blackwell)
-  d |= (uint64_t)2 << 61;                          // layout: SWIZZLE_128B
-  return d;
-}
-// Instruction descriptor: D f32, A/B bf16, both K-major, M=128, N=16.
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-
-AMUSD_DEV void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate));
-}
-AMUSD_DEV void umma_commit(uint32_t mbar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar) : "memory");
-}
-AMUSD_DEV void tmem_ld16(uint32_t taddr, float* v) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-AMUSD_DEV void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-// 32 consecutive fp32 accumulator columns of this thread's TMEM lane.
-AMUSD_DEV void tmem_ld32(uint32_t taddr, float* v) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
 
 // ------------------------------------------------------------ stream-K map
 struct Split {

@@ -370,8 +370,23 @@ class TransformerModel(CudaModel):
             out[n] = t
         return out
 
+    PATHS = {"persistent": L.PATH_PERSISTENT, "kernels": L.PATH_KERNELS, "simt": L.PATH_SIMT}
+
+    def set_path(self, path: str) -> None:
+        """Select the forward implementation (perf A/B, parity tests): 'persistent'
+        (one tcgen05 launch per forward, default), 'kernels' (per-kernel tcgen05)
+        or 'simt'.  Sessions capture the path when they first launch an engine."""
+        if path not in self.PATHS:
+            raise InvalidInputError(f"unknown forward path {path!r}")
+        L.check(self._lib.amusd_model_set_path(self._h, self.PATHS[path]))
+        self.path = path
+
     def kernels_per_forward(self) -> int:
-        return 1 + 5 * self.config.n_layers + 2
+        c = self.config
+        tc = c.dtype == "bf16" and c.use_tensor_cores
+        if tc and getattr(self, "path", "persistent") == "persistent":
+            return 1
+        return 1 + 5 * c.n_layers + 2
 
     def last_logits(self, rows: int = 1):
         """fp32 logits of the last `rows` forwarded rows of the latest API forward (parity/debug)."""

@@ -198,3 +198,40 @@ def test_tcgen05_llama8b_gemm_shapes():
     lb = simt.last_logits(len(cands)).numpy()
     assert _rel_err(la, lb) < 2 * BF16_LOGIT_TOL, _rel_err(la, lb)  # bf16 vs fp32 activations on both sides
     assert np.mean(np.array(a) == np.array(b)) >= 0.6
+
+
+def test_persistent_forward_matches_kernel_path():
+    """The one-launch persistent forward (forward_tc.cu) agrees with the per-kernel tcgen05
+    path (same arithmetic up to split-K order) and is run-to-run deterministic."""
+    TC = P.TransformerConfig
+    cands = [11, 22, 33, 44, 55, 66, 77, 88, 99, 111, 122, 133, 144, 155, 166]
+    for cfg, prompt in ((TC.tiny_verify(dtype="bf16", max_seq=320), PROMPT),
+                        (TC.tiny_draft(dtype="bf16", max_seq=320), PROMPT * 9),  # 288 positions: 2 attention splits
+                        (TC.llama_8b(max_seq=96, n_layers=2), PROMPT[:20])):
+        m = P.TransformerModel(cfg, seed=31)
+        runs = []
+        for path in ("persistent", "persistent", "kernels"):
+            m.set_path(path)
+            preds = m.verify_tokens(m.init_state(prompt), cands)
+            runs.append((preds, m.last_logits(len(cands)).numpy()))
+        (p0, l0), (p1, l1), (p2, l2) = runs
+        assert p0 == p1 and np.array_equal(l0, l1), "persistent forward is not deterministic"
+        assert _rel_err(l0, l2) < BF16_LOGIT_TOL, _rel_err(l0, l2)  # bf16 intermediates, different split-K order
+        assert np.mean(np.array(p0) == np.array(p2)) >= 0.9
+        del m
+    P.engines.clear_sessions()
+
+
+def test_persistent_forward_rows_invariant():
+    """A row's logits do not depend on how many rows share the persistent forward."""
+    TC = P.TransformerConfig
+    m = P.TransformerModel(TC.llama_1b(max_seq=96, n_layers=3), seed=32)
+    cands = [101, 202, 303, 404, 505, 606, 707]
+    m.verify_tokens(m.init_state(PROMPT[:24]), cands)
+    full = m.last_logits(len(cands)).numpy()
+    for k in (1, 3, 5):
+        m.verify_tokens(m.init_state(PROMPT[:24]), cands[:k])
+        part = m.last_logits(k).numpy()
+        assert np.array_equal(part, full[:k]), k
+    del m
+    P.engines.clear_sessions()
