@@ -126,7 +126,7 @@ static bool fw_enabled() {
 }
 static int fw_units() {
   static int v = -1;
-  if (v < 0) v = std::max(1, env_int("AMUSD_FW_UNITS", 8));
+  if (v < 0) v = std::max(1, env_int("AMUSD_FW_UNITS", 16));
   return v;
 }
 static int num_sms() {
@@ -392,6 +392,7 @@ static int fw_forward(amusd_model* m, StepCtl* ctl, cudaStream_t st, bool want_l
   // L2 prefetch window (bytes of weights ahead of the grab pointer), AMUSD_FW_L2_MB
   a.prefetch_items = (int)((size_t)env_int("AMUSD_FW_L2_MB", 0) * (1 << 20) / ((size_t)fw_units() * 16384));
   a.inflight = env_int("AMUSD_FW_INFLIGHT", 0);
+  a.prefetch_next = env_int("AMUSD_FW_PREFETCH_NEXT", 0);  // measured: L2 prefetch costs more than it hides
   a.debug = env_int("AMUSD_FW_DEBUG", 0);
   CUDA_TRY(fw::launch_forward(a, m->map_xa, m->map_attn, m->map_act, m->fw_grid, m->fw_stages, st));
   return AMUSD_OK;
@@ -927,13 +928,15 @@ static int capture_body(amusd_session* s, int engine, int actor, cudaGraph_t bod
   // verify forward at the same time, so each gets a ring that lets two CTAs
   // share an SM; every other engine owns the GPU (deepest ring, 1 CTA/SM).
   const bool colo = engine == AMUSD_ENGINE_ASYNC;
+  // Co-located AMUSD: the draft and the verify forward run at the same time on DISJOINT SM
+  // sets (each persistent CTA fills an SM; grids summing to <= #SMs can always co-run, and
+  // the work-queue kernel needs no particular grid size).  Other engines own the GPU.
+  const int draft_sms = std::max(1, std::min(num_sms() - 1, env_int("AMUSD_FW_DRAFT_GRID", 56)));
   for (amusd_model* m : {s->draft, s->verify}) {
     if (!m || !use_fw(m)) continue;
-    m->fw_stages = colo ? env_int("AMUSD_FW_COLO_STAGES", fw_max_stages(m->cfg, 2))
-                        : env_int("AMUSD_FW_STAGES", fw_max_stages(m->cfg, 1));
+    m->fw_stages = env_int("AMUSD_FW_STAGES", fw_max_stages(m->cfg, 1));
     m->fw_grid = num_sms();
-    if (colo && m == s->draft) m->fw_grid = std::max(1, std::min(num_sms(), env_int("AMUSD_FW_DRAFT_GRID", num_sms())));
-    if (colo && m == s->verify) m->fw_grid = std::max(1, std::min(num_sms(), env_int("AMUSD_FW_VERIFY_GRID", num_sms())));
+    if (colo) m->fw_grid = m == s->draft ? draft_sms : num_sms() - draft_sms;
   }
   auto fwd = [&](amusd_model* m, StepCtl* c, int nr) { if (!r) r = model_forward(m, c, nr, st, pdl, false); };
   auto pk = [&](int which, int arg) { if (!r && proto_launch(which, a, st, arg) != cudaSuccess) r = fail(AMUSD_ERR_CUDA, "protocol launch failed"); };

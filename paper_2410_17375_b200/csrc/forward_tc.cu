@@ -34,6 +34,9 @@
 // the same whatever the verify window size (AMUSD tokens == AR tokens).
 #include <cuda.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "forward_tc.h"
 #include "internal.h"
@@ -180,7 +183,7 @@ AMUSD_DEV int phase_count(const FwArgs& a, const Lay& L, int p) {
 struct GemmRes {
   const uint8_t* wt;
   const __nv_bfloat16* gnext;
-  int epi, map, kb, kc, nchunks, nitems;
+  int epi, map, kb, kc, nchunks, nitems, ntiles;
 };
 AMUSD_DEV GemmRes resolve(const FwArgs& a, int gk, int layer) {
   const GemmKind& g = a.g[gk];
@@ -188,6 +191,7 @@ AMUSD_DEV GemmRes resolve(const FwArgs& a, int gk, int layer) {
   r.wt = g.wt + (size_t)layer * g.wt_stride;
   r.gnext = g.gnext ? g.gnext + (size_t)layer * g.gnext_stride : nullptr;
   r.epi = g.epi; r.map = g.map; r.kb = g.kb; r.kc = g.kc; r.nchunks = g.nchunks; r.nitems = g.nitems;
+  r.ntiles = g.ntiles;
   return r;
 }
 
@@ -420,14 +424,21 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
           }
         }
       } else {
+        // this step's keys: SAME summation order as the cached path (a position's score
+        // must not depend on whether it is in the cache or the window: batch invariance)
         const float* kr = sm->kn[t - pos0];
-        for (int c = 0; c < HD; c += 4) {
-          const float4 kf = *(const float4*)&kr[c];
+#pragma unroll 4
+        for (int cc = 0; cc < NC; ++cc) {
+          const int c = (cc + tid) % NC;
+          const float4 ka = *(const float4*)&kr[8 * c], kb4 = *(const float4*)&kr[8 * c + 4];
+          const float f[8] = {ka.x, ka.y, ka.z, ka.w, kb4.x, kb4.y, kb4.z, kb4.w};
 #pragma unroll
           for (int j = 0; j < G; ++j) {
-            const float4 qa = *(const float4*)&sm->qs[j][c];
-            dot[j] = fmaf(kf.x, qa.x, dot[j]); dot[j] = fmaf(kf.y, qa.y, dot[j]);
-            dot[j] = fmaf(kf.z, qa.z, dot[j]); dot[j] = fmaf(kf.w, qa.w, dot[j]);
+            const float4 qa = *(const float4*)&sm->qs[j][8 * c], qb = *(const float4*)&sm->qs[j][8 * c + 4];
+            dot[j] = fmaf(f[0], qa.x, dot[j]); dot[j] = fmaf(f[1], qa.y, dot[j]);
+            dot[j] = fmaf(f[2], qa.z, dot[j]); dot[j] = fmaf(f[3], qa.w, dot[j]);
+            dot[j] = fmaf(f[4], qb.x, dot[j]); dot[j] = fmaf(f[5], qb.y, dot[j]);
+            dot[j] = fmaf(f[6], qb.z, dot[j]); dot[j] = fmaf(f[7], qb.w, dot[j]);
           }
         }
       }
@@ -635,9 +646,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
         const int kind = kind_of(pj.x, a.L);
         if (!is_gemm(kind)) return;
         const GemmRes g = resolve(a, gemm_of(kind), layer_of(pj.x));
-        const int t = pj.y / g.nchunks, c = pj.y - t * g.nchunks;
+        const int c = pj.y / g.ntiles, t = pj.y - c * g.ntiles;
         prefetch_l2(g.wt + ((size_t)t * g.kb + (size_t)c * g.kc) * kWBytes, (uint32_t)g.kc * kWBytes, pol_keep);
       };
+      if (a.prefetch_next) {  // layer 0's QKV + O slice of this CTA
+        const size_t span = a.qo_bytes;
+        const size_t lo = span * blockIdx.x / gridDim.x & ~(size_t)15, hi = span * (blockIdx.x + 1) / gridDim.x & ~(size_t)15;
+        if (hi > lo) prefetch_l2(a.g[kGQkv].wt + lo, (uint32_t)(hi - lo), pol_keep);
+      }
       if (ahead > 0)  // the first `ahead` items have no earlier grabber: spread them over the CTAs
         for (int k = blockIdx.x; k < ahead; k += gridDim.x) prefetch_item(k);
       int i_next = atomicAdd(a.sched, 1);  // grab counter: sched[0]; exit counter: sched[kPad]
@@ -660,9 +676,18 @@ __global__ void __launch_bounds__(kThreads, MINB)
         mbar_arrive(smem_u32(&qfull[slot]));
         ++n;
         const int kind = kind_of(pj.x, a.L);
+        if (kind == kKDown && a.prefetch_next && layer_of(pj.x) + 1 < a.L) {
+          // Move the next layer's QKV + O weights (the latency-bound part of its chain) to L2
+          // while this bandwidth-bound phase streams: down item j prefetches slice j.
+          const size_t span = a.qo_bytes, nslices = (size_t)a.g[kGDown].nitems;
+          const size_t lo = span * pj.y / nslices & ~(size_t)15, hi = span * (pj.y + 1) / nslices & ~(size_t)15;
+          if (hi > lo)
+            prefetch_l2(a.g[kGQkv].wt + (size_t)(layer_of(pj.x) + 1) * a.g[kGQkv].wt_stride + lo, (uint32_t)(hi - lo),
+                        pol_keep);
+        }
         if (is_gemm(kind)) {
           const GemmRes g = resolve(a, gemm_of(kind), layer_of(pj.x));
-          const int t = pj.y / g.nchunks, c = pj.y - t * g.nchunks;
+          const int c = pj.y / g.ntiles, t = pj.y - c * g.ntiles;  // chunk-major item order
           const uint8_t* src = g.wt + ((size_t)t * g.kb + (size_t)c * g.kc) * kWBytes;
           for (int u = 0; u < g.kc; ++u, ++gu, rg.next(S)) {
             const int s = rg.s;
@@ -707,7 +732,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         if (a.dbg) dbg_mark(a, phase_first(a, L, it.x) + it.y, 3, globaltimer());
         const GemmKind& g = a.g[gemm_of(kind)];
         const CUtensorMap* map = g.map == 0 ? &m_xa : (g.map == 1 ? &m_attn : &m_act);
-        const int c = it.y % g.nchunks, kc = g.kc;
+        const int c = it.y / g.ntiles, kc = g.kc;
         for (int u = 0; u < kc; ++u, rg.next(S)) {
           const int s = rg.s;
           mbar_wait_t(smem_u32(&empty[s]), rg.ph ^ 1u);
@@ -816,7 +841,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
           named_bar(1, 128);
           if (tid == 0) es->inv_phase = p;
         }
-        const int t = j / nchunks;
+        // Chunk-major order: item j = c * ntiles + t.  Every tile's chunk 0 is grabbed before
+        // any chunk 1, ..., so a tile's merging (last) chunk comes a full round after the
+        // chunks it waits for.
+        const int cj = j / g.ntiles, t = j - cj * g.ntiles;
         bool final = true;
         float acc[BN];
         if (nchunks > 1) {
@@ -832,7 +860,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           named_bar(1, 128);
           // The tile's last chunk (grabbed after its other chunks) merges; the others publish
           // with a fire-and-forget release and move on -- no round trip in their epilogue.
-          final = (j - t * nchunks) == nchunks - 1;
+          final = cj == nchunks - 1;
           if (!final) {
             if (tid == 0) red_add_release(a.tile_cnt + t * kPad, 1);
           } else {
@@ -886,7 +914,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
         }
         named_bar(1, 128);
         staged = asm_->last;
+        if (a.dbg && tid == 0) dbg_mark(a, phase_first(a, L, p) + j, 3, globaltimer());
         attn_item<HD, G>(a, asm_, staged, attn_par, layer, gh, r, split, L.pos0, tid);
+        if (a.dbg && tid == 0) dbg_mark(a, phase_first(a, L, p) + j, 4, globaltimer());
         if (staged) attn_par ^= 1u;
       }
       // publish: this item's writes are visible (generic and async proxy) before the count
@@ -941,15 +971,25 @@ static int pick_kc(int kb, int target) {
   return best;
 }
 
+// Units (16 KB) per work item of each GEMM kind; AMUSD_FW_UNITS_{QKV,O,GU,DOWN,LM} override.
+static int kind_units(const char* name, int dflt) {
+  char key[64];
+  snprintf(key, sizeof(key), "AMUSD_FW_UNITS_%s", name);
+  const char* e = getenv(key);
+  return (e && *e) ? atoi(e) : dflt;
+}
+
 void build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_floats, int* max_tiles) {
   const int ncols = (m.H + 2 * m.KV) * m.hd, hh = m.H * m.hd;
   const long long b_qkv = (long long)ncols * m.d * 2, b_o = (long long)m.d * hh * 2, b_gu = 2ll * m.ffn * m.d * 2;
   size_t wsf = 0;
   int mt = 0;
-  auto kind = [&](int epi, int map, int ntiles, int K, int N, int ldo, const uint8_t* wt, long long stride) {
+  auto kind = [&](int epi, int map, int ntiles, int K, int N, int ldo, const uint8_t* wt, long long stride,
+                  const char* name) {
     GemmKind g{};
     g.epi = epi; g.map = map; g.ntiles = ntiles; g.kb = K / BK;
-    g.kc = pick_kc(g.kb, units_per_item);
+    const bool chain = name[0] == 'Q' || (name[0] == 'O' && name[1] == 0);
+    g.kc = pick_kc(g.kb, kind_units(name, chain ? std::max(1, units_per_item / 2) : units_per_item));
     g.nchunks = g.kb / g.kc;
     g.nitems = ntiles * g.nchunks;
     g.N = N; g.ldo = ldo; g.wt = wt; g.wt_stride = stride;
@@ -958,21 +998,23 @@ void build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_f
     return g;
   };
   const uint8_t* w0 = m.wt_layer0;
-  a->g[kGQkv] = kind(kEpStoreScaled, 0, ncols / BM, m.d, ncols, ncols, w0, m.wt_layer_bytes);
+  // QKV / O sit on the latency-bound part of the layer chain: half-size items (measured best)
+  a->g[kGQkv] = kind(kEpStoreScaled, 0, ncols / BM, m.d, ncols, ncols, w0, m.wt_layer_bytes, "QKV");
   a->g[kGQkv].out = m.qkv;
-  a->g[kGO] = kind(kEpResid, 1, m.d / BM, hh, m.d, m.d, w0 + b_qkv, m.wt_layer_bytes);
+  a->g[kGO] = kind(kEpResid, 1, m.d / BM, hh, m.d, m.d, w0 + b_qkv, m.wt_layer_bytes, "O");
   a->g[kGO].out = m.h; a->g[kGO].xnext = m.xa;
   a->g[kGO].gnext = m.norms + m.d;          // mlp RMSNorm of layer l at 2l+1
   a->g[kGO].gnext_stride = 2 * m.d;
-  a->g[kGGu] = kind(kEpGateUp, 0, m.ffn / 64, m.d, m.ffn, m.ffn, w0 + b_qkv + b_o, m.wt_layer_bytes);
+  a->g[kGGu] = kind(kEpGateUp, 0, m.ffn / 64, m.d, m.ffn, m.ffn, w0 + b_qkv + b_o, m.wt_layer_bytes, "GU");
   a->g[kGGu].out_b = m.act_b;
-  a->g[kGDown] = kind(kEpResid, 2, m.d / BM, m.ffn, m.d, m.d, w0 + b_qkv + b_o + b_gu, m.wt_layer_bytes);
+  a->g[kGDown] = kind(kEpResid, 2, m.d / BM, m.ffn, m.d, m.d, w0 + b_qkv + b_o + b_gu, m.wt_layer_bytes, "DOWN");
   a->g[kGDown].out = m.h; a->g[kGDown].xnext = m.xa;
   a->g[kGDown].gnext = m.norms + 2 * m.d;   // attention RMSNorm of layer l+1 at 2l+2 (final norm at 2L)
   a->g[kGDown].gnext_stride = 2 * m.d;
-  a->g[kGLm] = kind(kEpArgmax, 0, m.vocab / BM, m.d, m.vocab, m.vocab, m.wt_lm, 0);
+  a->g[kGLm] = kind(kEpArgmax, 0, m.vocab / BM, m.d, m.vocab, m.vocab, m.wt_lm, 0, "LM");
   a->L = m.L;
   a->attn_max = attn_items_max(m.KV, m.S);
+  a->qo_bytes = (size_t)(b_qkv + b_o);
   *ws_floats = wsf;
   *max_tiles = mt;
 }

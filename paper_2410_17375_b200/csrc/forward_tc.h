@@ -65,6 +65,8 @@ struct FwArgs {
   float scale, eps;
   int stages;
   int prefetch_items;           // L2 prefetch distance in work items (0 = off)
+  int prefetch_next;            // DOWN items prefetch the next layer's QKV + O weights into L2
+  size_t qo_bytes;              // QKV + O tiled weight bytes of one layer (contiguous)
   int inflight;                 // max unlanded weight units per CTA (0 = ring depth)
   int debug;                    // perf-isolation bits (AMUSD_FW_DEBUG), 0 in production
   long long* dbg;               // optional per-item timeline [item][8] (perf analysis), null in production

@@ -222,16 +222,27 @@ def test_persistent_forward_matches_kernel_path():
     P.engines.clear_sessions()
 
 
-def test_persistent_forward_rows_invariant():
-    """A row's logits do not depend on how many rows share the persistent forward."""
+@pytest.mark.parametrize("plen", [24, 126, 200, 300])
+def test_persistent_forward_rows_invariant(plen):
+    """A row's logits do not depend on how many rows share the persistent forward
+    (prefixes crossing the 128-position attention split boundaries included)."""
     TC = P.TransformerConfig
-    m = P.TransformerModel(TC.llama_1b(max_seq=96, n_layers=3), seed=32)
+    m = P.TransformerModel(TC.llama_1b(max_seq=352, n_layers=3), seed=32)
+    prompt = (PROMPT * 10)[:plen]
     cands = [101, 202, 303, 404, 505, 606, 707]
-    m.verify_tokens(m.init_state(PROMPT[:24]), cands)
+    m.verify_tokens(m.init_state(prompt), cands)
     full = m.last_logits(len(cands)).numpy()
     for k in (1, 3, 5):
-        m.verify_tokens(m.init_state(PROMPT[:24]), cands[:k])
+        m.verify_tokens(m.init_state(prompt), cands[:k])
         part = m.last_logits(k).numpy()
-        assert np.array_equal(part, full[:k]), k
+        assert np.array_equal(part, full[:k]), (plen, k, float(np.abs(part - full[:k]).max()))
+    # incremental: advancing row by row (AR-style) gives the same last-row logits
+    st = m.init_state(prompt)
+    for j, c in enumerate(cands[:4]):
+        m.next_token(st)
+        m.advance(st, [c])
+    m.next_token(st)
+    inc = m.last_logits(1).numpy()[0]
+    assert np.array_equal(inc, full[4]), (plen, float(np.abs(inc - full[4]).max()))
     del m
     P.engines.clear_sessions()
