@@ -97,12 +97,16 @@ struct amusd_model {
   std::vector<const uint8_t*> wt_qkv, wt_o, wt_gu, wt_d;
   const uint8_t* wt_lm = nullptr;
   uint8_t* tiled = nullptr;
-  CUtensorMap map_xa{}, map_attn{}, map_act{};
+  CUtensorMap map_xa{}, map_attn{}, map_act{}, map_xb{};
   // persistent forward (forward_tc.cu): phase table + self-resetting schedule
   fw::FwArgs fw_args{};           // schedule (GEMM kinds) + model pointers, built at create
   bool fw_ready = false;
   __nv_bfloat16* fw_norms = nullptr;  // packed RMSNorm weights [2L+1][d]
   float* fw_attn_ws = nullptr;        // attention split partials (128-position chunks)
+  __nv_bfloat16* fw_xb = nullptr;     // gate/up input (double buffer of xa_b)
+  float* fw_sspb = nullptr;
+  long long* fw_tflag = nullptr;      // per-tile completion stamps
+  int* fw_agrp = nullptr;             // attention items finished per (layer, head group)
   int* fw_attn_cnt = nullptr;
   int* fw_sched = nullptr;
   unsigned long long* fw_best = nullptr;
@@ -151,17 +155,20 @@ static int fw_max_stages(const amusd_tf_config& c, int per_sm) {
 static bool tc_shapes_ok(const amusd_tf_config* c) {
   const int ncols = (c->n_heads + 2 * c->n_kv_heads) * c->head_dim;
   // tcgen05 tiles: 128 weight rows (64 gate + 64 up features) x 64 K per unit
+  // and a QKV group block [q(G heads) | k | v] spans whole 128-row tiles
+  const int G = c->n_kv_heads ? c->n_heads / c->n_kv_heads : 0;
   return c->dtype == AMUSD_BF16 && c->use_tensor_cores && c->d_model % 128 == 0 && ncols % 128 == 0 &&
-         c->ffn % 64 == 0 && c->vocab % 128 == 0 && (c->n_heads * c->head_dim) % 64 == 0;
+         c->ffn % 64 == 0 && c->vocab % 128 == 0 && (c->n_heads * c->head_dim) % 64 == 0 &&
+         ((G + 2) * c->head_dim) % 128 == 0;
 }
 
 // Split-K workspace sizes of a config (dry run of build_kinds without pointers).
-static void fw_sizes(const amusd_tf_config* c, size_t* ws_floats, int* max_tiles) {
+static void fw_sizes(const amusd_tf_config* c, size_t* ws_floats, int* cnt_ints, int* max_tiles) {
   fw::ModelView v{};
   v.d = c->d_model; v.H = c->n_heads; v.KV = c->n_kv_heads; v.hd = c->head_dim; v.ffn = c->ffn; v.vocab = c->vocab;
   v.L = c->n_layers; v.S = c->max_seq;
   fw::FwArgs a{};
-  fw::build_kinds(v, fw_units(), &a, ws_floats, max_tiles);
+  fw::build_kinds(v, fw_units(), &a, ws_floats, cnt_ints, max_tiles);
 }
 
 static size_t tf_carve(const amusd_tf_config* c, void* base, amusd_model* m) {
@@ -208,16 +215,25 @@ static size_t tf_carve(const amusd_tf_config* c, void* base, amusd_model* m) {
   float* fws = nullptr;
   int* fcnt = nullptr;
   __nv_bfloat16* fnorms = nullptr;
+  __nv_bfloat16* fxb = nullptr;
+  float* fsspb = nullptr;
+  long long* ftflag = nullptr;
+  int* fagrp = nullptr;
   float* fattn_ws = nullptr;
   int* fattn_cnt = nullptr;
   if (tc) {
     int mt;
     size_t wsf;
-    fw_sizes(c, &wsf, &mt);
-    fsched = cv.take<int>((size_t)(2 + fw::num_phases(c->n_layers)) * fw::kCounterInts);
+    int cints;
+    fw_sizes(c, &wsf, &cints, &mt);
+    fsched = cv.take<int>(fw::sched_ints(c->n_layers));
     fbest = cv.take<unsigned long long>(KMAX);
     fws = cv.take<float>(std::max<size_t>(wsf, 1));
-    fcnt = cv.take<int>((size_t)std::max(mt, 1) * fw::kCounterInts);
+    fcnt = cv.take<int>((size_t)cints);
+    fxb = cv.take<__nv_bfloat16>((size_t)KMAX * c->d_model);
+    fsspb = cv.take<float>((size_t)KMAX * (c->d_model / 128));
+    ftflag = cv.take<long long>((size_t)4 * mt * (fw::kCounterInts / 2));
+    fagrp = cv.take<int>((size_t)c->n_layers * c->n_kv_heads * fw::kCounterInts);
     fnorms = cv.take<__nv_bfloat16>((size_t)(2 * c->n_layers + 1) * c->d_model);
     fattn_ws = cv.take<float>((size_t)c->n_kv_heads * KMAX * fw::attn_splits(c->max_seq) * group * (c->head_dim + 2));
     fattn_cnt = cv.take<int>((size_t)c->n_kv_heads * KMAX * fw::kCounterInts);
@@ -226,6 +242,7 @@ static size_t tf_carve(const amusd_tf_config* c, void* base, amusd_model* m) {
     m->attn_ws = attn_ws; m->attn_cnt = attn_cnt;
     m->fw_sched = fsched; m->fw_best = fbest; m->fw_ws = fws; m->fw_tile_cnt = fcnt; m->fw_norms = fnorms;
     m->fw_attn_ws = fattn_ws; m->fw_attn_cnt = fattn_cnt;
+    m->fw_xb = fxb; m->fw_sspb = fsspb; m->fw_tflag = ftflag; m->fw_agrp = fagrp;
     m->tc = tc; m->xa_b = xa_b; m->attn_b = attn_b; m->act_b = act_b; m->inv = inv; m->ssp = ssp_b; m->tc_ws = ws; m->tc_cnt = cnt; m->tiled = tiled;
     m->seq = seq; m->tok = tok; m->api_ctl = ctl; m->kc = kc; m->vc = vc; m->h = h; m->qkv = qkv;
     m->attn = attn; m->act = act; m->part = part; m->logits = logits; m->lm_grid = lm_grid;
@@ -333,6 +350,7 @@ static int tc_kernel(amusd_model* m, StepCtl* ctl, int l, int which, cudaStream_
       at.cos = m->w.rope_cos; at.sin = m->w.rope_sin; at.out = nullptr; at.out_b = m->attn_b; at.ldo = H * hd;
       at.H = H; at.KV = KV; at.hd = hd; at.S = c.max_seq; at.scale = 1.0f / sqrtf((float)hd);
       at.ws = m->attn_ws; at.counters = m->attn_cnt; at.max_splits = attn_max_splits(c.max_seq);
+      at.blocked = 1;  // the tensor-core QKV tiles are group-blocked
       CUDA_TRY(launch_attention(c.dtype, at, st, pdl));
       break;
     }
@@ -382,6 +400,7 @@ static int fw_forward(amusd_model* m, StepCtl* ctl, cudaStream_t st, bool want_l
   a.ctl = ctl; a.sched = m->fw_sched;
   a.embed = (const __nv_bfloat16*)m->w.embed; a.norms = m->fw_norms;
   a.h = m->h; a.xa = m->xa_b; a.ssp = m->ssp; a.qkv = m->qkv; a.attn_b = m->attn_b;
+  a.xb = m->fw_xb; a.sspb = m->fw_sspb; a.tflag = m->fw_tflag; a.agrp = m->fw_agrp;
   a.kcache = (char*)m->kc; a.vcache = (char*)m->vc; a.kv_layer_bytes = (long long)m->kv_layer_elems * 2;
   a.ws = m->fw_ws; a.tile_cnt = m->fw_tile_cnt; a.attn_ws = m->fw_attn_ws; a.attn_cnt = m->fw_attn_cnt;
   a.cos = m->w.rope_cos; a.sin = m->w.rope_sin; a.best = m->fw_best; a.logits = want_logits ? m->logits : nullptr;
@@ -394,7 +413,8 @@ static int fw_forward(amusd_model* m, StepCtl* ctl, cudaStream_t st, bool want_l
   a.inflight = env_int("AMUSD_FW_INFLIGHT", 0);
   a.prefetch_next = env_int("AMUSD_FW_PREFETCH_NEXT", 0);  // measured: L2 prefetch costs more than it hides
   a.debug = env_int("AMUSD_FW_DEBUG", 0);
-  CUDA_TRY(fw::launch_forward(a, m->map_xa, m->map_attn, m->map_act, m->fw_grid, m->fw_stages, st));
+  a.fine = env_int("AMUSD_FW_FINE", 0);  // per-tile deps measured slower: CTAs run their queues in order
+  CUDA_TRY(fw::launch_forward(a, m->map_xa, m->map_attn, m->map_act, m->map_xb, m->fw_grid, m->fw_stages, st));
   return AMUSD_OK;
 }
 
@@ -469,14 +489,16 @@ int amusd_tf_create(amusd_model** out, const amusd_tf_config* cfg, const amusd_t
     bool ok = true;
     uint8_t* p = m->tiled;
     cudaError_t e = cudaSuccess;
-    auto place = [&](const void* src, const void* src2, int N, int K) -> const uint8_t* {
+    auto place = [&](const void* src, const void* src2, int N, int K, bool qkv = false) -> const uint8_t* {
       const uint8_t* at = p;
-      if (e == cudaSuccess) e = tc::launch_tile_weights(src, src2, p, N, K, 0);
+      if (e == cudaSuccess)
+        e = qkv ? tc::launch_tile_weights(src, src2, p, N, K, 0, c.n_heads, c.n_kv_heads, c.head_dim)
+                : tc::launch_tile_weights(src, src2, p, N, K, 0);
       p += tc::tiled_bytes(src2 ? 2 * N : N, K);
       return at;
     };
     for (int l = 0; l < c.n_layers; ++l) {
-      m->wt_qkv.push_back(place(w->wqkv[l], nullptr, ncols, d));
+      m->wt_qkv.push_back(place(w->wqkv[l], nullptr, ncols, d, true));  // group-blocked q|k|v
       m->wt_o.push_back(place(w->wo[l], nullptr, d, hh));
       m->wt_gu.push_back(place(w->wgate[l], w->wup[l], c.ffn, d));
       m->wt_d.push_back(place(w->wdown[l], nullptr, d, c.ffn));
@@ -498,9 +520,10 @@ int amusd_tf_create(amusd_model** out, const amusd_tf_config* cfg, const amusd_t
       v.wt_layer_bytes = c.n_layers > 1 ? (long long)(m->wt_qkv[1] - m->wt_qkv[0]) : 0;
       v.wt_lm = m->wt_lm; v.norms = m->fw_norms;
       v.h = m->h; v.qkv = m->qkv; v.xa = m->xa_b; v.act_b = m->act_b;
+      v.xb = m->fw_xb; v.ssp = m->ssp; v.sspb = m->fw_sspb;
       size_t wsf;
-      int mt;
-      fw::build_kinds(v, fw_units(), &m->fw_args, &wsf, &mt);
+      int mt, cints;
+      fw::build_kinds(v, fw_units(), &m->fw_args, &wsf, &cints, &mt);
       m->fw_ready = e == cudaSuccess;
       m->fw_grid = num_sms();
       m->fw_stages = env_int("AMUSD_FW_STAGES", fw_max_stages(c, 1));
@@ -509,6 +532,7 @@ int amusd_tf_create(amusd_model** out, const amusd_tf_config* cfg, const amusd_t
     ok &= tc::make_map(&m->map_xa, m->xa_b, KMAX, d, KMAX);
     ok &= tc::make_map(&m->map_attn, m->attn_b, KMAX, hh, KMAX);
     ok &= tc::make_map(&m->map_act, m->act_b, KMAX, c.ffn, KMAX);
+    ok &= tc::make_map(&m->map_xb, m->fw_xb, KMAX, d, KMAX);
     if (!ok || e != cudaSuccess) {
       delete m;
       return fail(AMUSD_ERR_CUDA, std::string("tcgen05 path setup failed: ") +

@@ -97,6 +97,17 @@ AMUSD_DEV float warp_max(float v) {
   return v;
 }
 
+// ---- QKV group-block layout ----------------------------------------------------
+// Output column n of the blocked QKV projection -> row of the natural [q|k|v]
+// weight: block g = [q heads g*G..g*G+G-1 | k head g | v head g], (G+2)*hd wide.
+__host__ __device__ inline int qkv_group_row(int n, int H, int KV, int hd) {
+  const int G = H / KV, bw = (G + 2) * hd;
+  const int g = n / bw, w = n - g * bw;
+  if (w < G * hd) return g * G * hd + w;
+  if (w < (G + 1) * hd) return H * hd + g * hd + (w - G * hd);
+  return (H + KV) * hd + g * hd + (w - (G + 1) * hd);
+}
+
 // ---- element loads -----------------------------------------------------------
 template <typename T> struct Elem;
 template <> struct Elem<float> {

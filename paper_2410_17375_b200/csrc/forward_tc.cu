@@ -128,6 +128,38 @@ AMUSD_DEV void prefetch_l2(const void* src, uint32_t bytes, uint64_t policy) {
                : "memory");
 }
 
+AMUSD_DEV long long ld_acquire_gpu64(const long long* p) {
+  long long v;
+  asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+AMUSD_DEV void st_release_gpu64(long long* p, long long v) {
+  asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// Wait until every flag in [t0, t1) of a producer kind carries at least `stamp`:
+// all flags are loaded at once (one round trip when they are already set),
+// then only the missing ones are polled.
+AMUSD_DEV void wait_tiles(const long long* flags, int t0, int t1, long long stamp) {
+  constexpr int kBatch = 16;
+  for (int b0 = t0; b0 < t1; b0 += kBatch) {
+    long long v[kBatch];
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i)
+      v[i] = b0 + i < t1 ? ld_acquire_gpu64(flags + (size_t)(b0 + i) * (kCounterInts / 2)) : stamp;
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+      if (v[i] >= stamp) continue;
+      const long long* f = flags + (size_t)(b0 + i) * (kCounterInts / 2);
+      const long long t_start = globaltimer();
+      for (;;) {
+        __nanosleep(a_poll_ns);
+        if (ld_acquire_gpu64(f) >= stamp) break;
+        if (globaltimer() - t_start > kWaitNs) __trap();
+      }
+    }
+  }
+}
+
 // Ring cursor: stage index + phase parity, advanced incrementally (no division).
 struct Ring {
   int s = 0;
@@ -233,7 +265,7 @@ AMUSD_DEV void tile_epilogue(const FwArgs& a, const GemmKind& ph, const __nv_bfl
     named_bar(1, 128);
     if (q == 0 && lane < BN) {  // fixed order over the 4 lane quarters
       const float tot = es->sq[0 * BN + lane] + es->sq[1 * BN + lane] + es->sq[2 * BN + lane] + es->sq[3 * BN + lane];
-      __stcg(a.ssp + (size_t)lane * (a.d / BM) + t, lane < rows ? tot : 0.f);
+      __stcg(ph.ssp_out + (size_t)lane * (a.d / BM) + t, lane < rows ? tot : 0.f);
     }
   } else if (ph.epi == kEpGateUp) {
     // lanes 0..63: gate rows, 64..127: up rows of the same 64 features
@@ -365,9 +397,10 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
   const int lo = split * kAttnChunk, hi = min(p + 1, lo + kAttnChunk);
   const int half = HD / 2, ncols = (a.H + 2 * a.KV) * HD;
   const float* qkv = a.qkv;
+  const int qoff = g * (G + 2) * HD, koff = qoff + G * HD, voff = koff + HD;  // group-blocked q|k|v
   for (int i = tid; i < G * half; i += 128) {
     const int j = i / half, e = i - j * half;
-    const float* q = qkv + (size_t)r * ncols + (g * G + j) * HD;
+    const float* q = qkv + (size_t)r * ncols + qoff + j * HD;
     const float c = a.cos[(size_t)p * half + e], s = a.sin[(size_t)p * half + e];
     const float q0 = __ldcg(q + e), q1 = __ldcg(q + e + half);
     sm->qs[j][e] = q0 * c - q1 * s;
@@ -377,7 +410,7 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
   for (int i = tid; i < (jmax + 1) * half; i += 128) {
     const int j = i / half, e = i - j * half;
     const int pj = pos0 + j;
-    const float* kr = qkv + (size_t)j * ncols + (a.H + g) * HD;
+    const float* kr = qkv + (size_t)j * ncols + koff;
     const float c = a.cos[(size_t)pj * half + e], s = a.sin[(size_t)pj * half + e];
     const float k0 = __ldcg(kr + e), k1 = __ldcg(kr + e + half);
     sm->kn[j][e] = __bfloat162float(__float2bfloat16(k0 * c - k1 * s));
@@ -385,7 +418,7 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
   }
   for (int i = tid; i < (jmax + 1) * HD; i += 128) {
     const int j = i / HD, e = i - j * HD;
-    sm->vn[j][e] = __bfloat162float(__float2bfloat16(__ldcg(qkv + (size_t)j * ncols + (a.H + a.KV + g) * HD + e)));
+    sm->vn[j][e] = __bfloat162float(__float2bfloat16(__ldcg(qkv + (size_t)j * ncols + voff + e)));
   }
   if (staged) mbar_wait_t(smem_u32(&sm->bar), bar_par);
   named_bar(1, 128);
@@ -565,7 +598,8 @@ constexpr int epi_bytes() { return ((int)sizeof(EpiSmem) + 127) & ~127; }
 template <int HD, int G, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
     k_forward(const __grid_constant__ CUtensorMap m_xa, const __grid_constant__ CUtensorMap m_attn,
-              const __grid_constant__ CUtensorMap m_act, const __grid_constant__ FwArgs a) {
+              const __grid_constant__ CUtensorMap m_act, const __grid_constant__ CUtensorMap m_xb,
+              const __grid_constant__ FwArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int S = a.stages;
@@ -584,7 +618,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
   uint64_t* qempty = qfull + kQ;
   int2* queue = (int2*)(qempty + kQ);
   uint32_t* tmem_slot = (uint32_t*)(queue + kQ);
-  int* s_lay = (int*)(tmem_slot + 1);  // A, rows, pos0, active
+  int* s_lay = (int*)(tmem_slot + 1);  // A, rows, pos0, active, epoch
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -597,6 +631,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     s_lay[1] = rows;
     s_lay[2] = pos0;
     s_lay[3] = active;
+    s_lay[4] = ld_volatile(a.sched + 2 * kPad);  // launch epoch (bumped by the last CTA of each launch)
     for (int s = 0; s < S; ++s) {
       mbar_init(smem_u32(&wfull[s]), 1);
       mbar_init(smem_u32(&xfull[s]), 1);
@@ -627,7 +662,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  int* done = a.sched + 2 * kPad;  // done count of phase p at done[p * kPad]
+  int* done = a.sched + 3 * kPad;  // done count of phase p at done[p * kPad]
+  // Per-tile completion stamps: epoch * 2^16 + layer + 1 (monotonic: never reset).
+  const long long epoch_base = (long long)s_lay[4] << 16;
+  auto stamp = [&](int layer) { return epoch_base + layer + 1; };
+  auto flags_of = [&](int gk) { return a.tflag + (size_t)gk * a.tflag_tiles * (kPad / 2); };
 
   if (warp == 0) {
     // ===== scheduler + weight producer =====
@@ -723,16 +762,35 @@ __global__ void __launch_bounds__(kThreads, MINB)
         if (it.x < 0) break;
         const int kind = kind_of(it.x, a.L);
         if (!is_gemm(kind)) continue;
-        const int dep = it.x - 1;
-        if (dep > dep_ok && !(a.debug & 2)) {  // debug bit 1: ignore GEMM dependencies (timing only)
-          wait_count(done + dep * kPad, phase_count(a, L, dep));
+        const GemmKind& g = a.g[gemm_of(kind)];
+        const int c = it.y / g.ntiles, kc = g.kc, layer = layer_of(it.x);
+        const int prod = it.x - 1;  // producer phase
+        if (!(a.debug & 2) && prod > dep_ok) {  // debug bit 1: ignore GEMM dependencies (timing only)
+          // Fine-grained: wait only for the producer tiles covering this item's K range --
+          // unless the whole producer phase is already known (or now seen) complete.
+          const int k0 = c * kc * BK, k1 = k0 + kc * BK;  // input columns [k0, k1)
+          if (!a.fine) {  // phase-level dependency (default, measured faster)
+            wait_count(done + prod * kPad, phase_count(a, L, prod));
+            dep_ok = prod;
+          } else if (ld_acquire_gpu(done + prod * kPad) >= phase_count(a, L, prod)) {
+            dep_ok = prod;
+          } else if (kind == kKQkv && layer == 0) {
+            wait_count(done, KMAX);  // embedding rows
+          } else if (kind == kKQkv || kind == kKLm) {  // xa <- down(layer-1) tiles (128 columns each)
+            wait_tiles(flags_of(kGDown), k0 / BM, (k1 + BM - 1) / BM, stamp(kind == kKLm ? a.L - 1 : layer - 1));
+          } else if (kind == kKO) {  // attn_b columns -> heads -> head groups of this layer
+            const int g0 = k0 / a.hd / (a.H / a.KV), g1 = ((k1 + a.hd - 1) / a.hd + a.H / a.KV - 1) / (a.H / a.KV);
+            const int per_group = L.A / a.KV;
+            for (int gg = g0; gg < g1; ++gg) wait_count(a.agrp + ((size_t)layer * a.KV + gg) * kPad, per_group);
+          } else if (kind == kKGu) {  // xb <- O(layer) tiles
+            wait_tiles(flags_of(kGO), k0 / BM, (k1 + BM - 1) / BM, stamp(layer));
+          } else {  // down: act features [k0, k1) <- gate/up tiles of 64 features
+            wait_tiles(flags_of(kGGu), k0 / 64, (k1 + 63) / 64, stamp(layer));
+          }
           fence_proxy_async();
-          dep_ok = dep;
         }
         if (a.dbg) dbg_mark(a, phase_first(a, L, it.x) + it.y, 3, globaltimer());
-        const GemmKind& g = a.g[gemm_of(kind)];
-        const CUtensorMap* map = g.map == 0 ? &m_xa : (g.map == 1 ? &m_attn : &m_act);
-        const int c = it.y / g.ntiles, kc = g.kc;
+        const CUtensorMap* map = g.map == 0 ? &m_xa : (g.map == 1 ? &m_attn : (g.map == 2 ? &m_act : &m_xb));
         for (int u = 0; u < kc; ++u, rg.next(S)) {
           const int s = rg.s;
           mbar_wait_t(smem_u32(&empty[s]), rg.ph ^ 1u);
@@ -791,7 +849,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     const int nl = q * 32 + lane;  // tile row held by this thread
     EpiSmem* es = (EpiSmem*)(scratch + kAttnBytes);  // never aliased by the attention scratch
     if (tid == 0) es->inv_phase = -1;
-    int n = 0, seg = 0, dep_ok = -1;
+    int n = 0, seg = 0, attn_dep_ok = -1;
     uint32_t attn_par = 0;
     for (;;) {
       const int slot = n % kQ;
@@ -829,10 +887,20 @@ __global__ void __launch_bounds__(kThreads, MINB)
         // RMSNorm scale of the phase's input rows (once per phase per CTA)
         const bool need_inv = epi == kEpStoreScaled || epi == kEpGateUp || epi == kEpArgmax;
         if (need_inv && es->inv_phase != p) {
+          // the RMSNorm scale needs the whole input row: wait for the full producer phase
+          // (the MMA above only needed the tiles of its K range)
+          if (a.fine) {  // (phase-level mode: the MMA already waited for the whole phase)
+            if (tid == 0) {
+              const int prod = p - 1;  // O(l) for gate/up; down(l-1) for QKV(l); down(L-1) for the LM head
+              wait_count(done + prod * kPad, phase_count(a, L, prod));
+            }
+            named_bar(1, 128);
+          }
           // 8 threads per row, each a strided slice of the row's tile sums; fixed shuffle tree
+          const float* ssp_in = g.ssp_in;
           const int nt = a.d / BM, rr = tid >> 3, part = tid & 7;
           float tot = 0.f;
-          for (int k = part; k < nt; k += 8) tot += __ldcg(a.ssp + (size_t)rr * nt + k);
+          for (int k = part; k < nt; k += 8) tot += __ldcg(ssp_in + (size_t)rr * nt + k);
           tot += __shfl_xor_sync(0xffffffffu, tot, 1);
           tot += __shfl_xor_sync(0xffffffffu, tot, 2);
           tot += __shfl_xor_sync(0xffffffffu, tot, 4);
@@ -851,7 +919,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           // Split-K in exact int64 fixed point (2^-32): the red.adds commute, so the merged
           // tile is bit-identical whatever the chunks' arrival order (deterministic, batch
           // invariant) and no partial ever needs a merge round trip.  Layout [tile][row][128].
-          unsigned long long* acc64 = (unsigned long long*)a.ws + (size_t)t * BN * BM + nl;
+          unsigned long long* acc64 = (unsigned long long*)a.ws + g.ws_off + (size_t)t * BN * BM + nl;
 #pragma unroll
           for (int r = 0; r < BN; ++r) {
             const long long fx = __float2ll_rn(v[r] * 4294967296.0f);
@@ -862,11 +930,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
           // with a fire-and-forget release and move on -- no round trip in their epilogue.
           final = cj == nchunks - 1;
           if (!final) {
-            if (tid == 0) red_add_release(a.tile_cnt + t * kPad, 1);
+            if (tid == 0) red_add_release(a.tile_cnt + g.cnt_off + t * kPad, 1);
           } else {
             if (tid == 0) {
-              wait_count(a.tile_cnt + t * kPad, nchunks - 1);
-              a.tile_cnt[t * kPad] = 0;  // re-arm for the next phase / launch
+              wait_count(a.tile_cnt + g.cnt_off + t * kPad, nchunks - 1);
+              a.tile_cnt[g.cnt_off + t * kPad] = 0;  // re-arm for the next phase / launch
             }
             named_bar(1, 128);
             long long s64[BN];
@@ -907,11 +975,15 @@ __global__ void __launch_bounds__(kThreads, MINB)
           staged = attn_prefetch<HD, G>(a, asm_, layer, gh, lo, hi, L.pos0);
           asm_->last = staged;
         }
-        const int dep = p - 1;
-        if (dep > dep_ok) {
-          if (tid == 0) wait_count(done + dep * kPad, phase_count(a, L, dep));
-          dep_ok = dep;
+        if (tid == 0) {
+          if (a.fine) {  // this head group's QKV tiles only (group-blocked: consecutive tiles)
+            const int tpg = (G + 2) * HD / BM;
+            wait_tiles(flags_of(kGQkv), gh * tpg, (gh + 1) * tpg, stamp(layer));
+          } else if (p - 1 > attn_dep_ok) {
+            wait_count(done + (p - 1) * kPad, phase_count(a, L, p - 1));
+          }
         }
+        attn_dep_ok = p - 1;
         named_bar(1, 128);
         staged = asm_->last;
         if (a.dbg && tid == 0) dbg_mark(a, phase_first(a, L, p) + j, 3, globaltimer());
@@ -934,6 +1006,21 @@ __global__ void __launch_bounds__(kThreads, MINB)
             }
           }
         } else if (wrote) {
+          if (!a.fine) {
+          } else if (is_gemm(kind)) {  // tile final: stamp it for the fine-grained consumers
+            const int gk = gemm_of(kind);
+            const int t = j % a.g[gk].ntiles;
+            st_release_gpu64(flags_of(gk) + (size_t)t * (kPad / 2), stamp(layer));
+          } else if (kind == kKAttn) {
+            int r = 0, rem = j;
+            for (;;) {
+              const int cnt = a.KV * nsplit_of(L.pos0 + r);
+              if (rem < cnt) break;
+              rem -= cnt;
+              ++r;
+            }
+            red_add_release(a.agrp + ((size_t)layer * a.KV + rem % a.KV) * kPad, 1);
+          }
           red_add_release(done + p * kPad, 1);
         } else {
           // non-final split-K item: its partial was released by the tile count; the consumers'
@@ -955,6 +1042,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
       a.sched[0] = 0;
       a.sched[kPad] = 0;
       for (int i = 0; i < num_phases(a.L); ++i) done[i * kPad] = 0;
+      for (int i = 0; i < a.L * a.KV; ++i) a.agrp[(size_t)i * kPad] = 0;
+      a.sched[2 * kPad] = s_lay[4] + 1;  // next launch's epoch (tile stamps stay monotonic)
       __threadfence();
     }
   }
@@ -979,11 +1068,11 @@ static int kind_units(const char* name, int dflt) {
   return (e && *e) ? atoi(e) : dflt;
 }
 
-void build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_floats, int* max_tiles) {
+void build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_floats, int* cnt_ints, int* max_tiles) {
   const int ncols = (m.H + 2 * m.KV) * m.hd, hh = m.H * m.hd;
   const long long b_qkv = (long long)ncols * m.d * 2, b_o = (long long)m.d * hh * 2, b_gu = 2ll * m.ffn * m.d * 2;
-  size_t wsf = 0;
-  int mt = 0;
+  long long ws = 0;  // int64 elements
+  int cnt = 0, mt = 0;
   auto kind = [&](int epi, int map, int ntiles, int K, int N, int ldo, const uint8_t* wt, long long stride,
                   const char* name) {
     GemmKind g{};
@@ -993,29 +1082,38 @@ void build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_f
     g.nchunks = g.kb / g.kc;
     g.nitems = ntiles * g.nchunks;
     g.N = N; g.ldo = ldo; g.wt = wt; g.wt_stride = stride;
-    if (g.nchunks > 1) wsf = std::max(wsf, (size_t)g.ntiles * BM * BN * 2);  // int64 accumulator tiles
-    mt = std::max(mt, ntiles);
+    // every kind owns its accumulators / counters: consecutive phases overlap under the
+    // fine-grained dependencies
+    g.ws_off = ws;
+    g.cnt_off = cnt;
+    if (g.nchunks > 1) ws += (long long)ntiles * BM * BN;
+    cnt += ntiles * kCounterInts;
+    if (epi != kEpArgmax) mt = std::max(mt, ntiles);
     return g;
   };
   const uint8_t* w0 = m.wt_layer0;
-  // QKV / O sit on the latency-bound part of the layer chain: half-size items (measured best)
   a->g[kGQkv] = kind(kEpStoreScaled, 0, ncols / BM, m.d, ncols, ncols, w0, m.wt_layer_bytes, "QKV");
   a->g[kGQkv].out = m.qkv;
+  a->g[kGQkv].ssp_in = m.ssp;
   a->g[kGO] = kind(kEpResid, 1, m.d / BM, hh, m.d, m.d, w0 + b_qkv, m.wt_layer_bytes, "O");
-  a->g[kGO].out = m.h; a->g[kGO].xnext = m.xa;
+  a->g[kGO].out = m.h; a->g[kGO].xnext = m.xb; a->g[kGO].ssp_out = m.sspb;  // -> gate/up (double buffer)
   a->g[kGO].gnext = m.norms + m.d;          // mlp RMSNorm of layer l at 2l+1
   a->g[kGO].gnext_stride = 2 * m.d;
-  a->g[kGGu] = kind(kEpGateUp, 0, m.ffn / 64, m.d, m.ffn, m.ffn, w0 + b_qkv + b_o, m.wt_layer_bytes, "GU");
+  a->g[kGGu] = kind(kEpGateUp, 3, m.ffn / 64, m.d, m.ffn, m.ffn, w0 + b_qkv + b_o, m.wt_layer_bytes, "GU");
   a->g[kGGu].out_b = m.act_b;
+  a->g[kGGu].ssp_in = m.sspb;
   a->g[kGDown] = kind(kEpResid, 2, m.d / BM, m.ffn, m.d, m.d, w0 + b_qkv + b_o + b_gu, m.wt_layer_bytes, "DOWN");
-  a->g[kGDown].out = m.h; a->g[kGDown].xnext = m.xa;
+  a->g[kGDown].out = m.h; a->g[kGDown].xnext = m.xa; a->g[kGDown].ssp_out = m.ssp;  // -> next QKV / LM head
   a->g[kGDown].gnext = m.norms + 2 * m.d;   // attention RMSNorm of layer l+1 at 2l+2 (final norm at 2L)
   a->g[kGDown].gnext_stride = 2 * m.d;
   a->g[kGLm] = kind(kEpArgmax, 0, m.vocab / BM, m.d, m.vocab, m.vocab, m.wt_lm, 0, "LM");
+  a->g[kGLm].ssp_in = m.ssp;
   a->L = m.L;
   a->attn_max = attn_items_max(m.KV, m.S);
   a->qo_bytes = (size_t)(b_qkv + b_o);
-  *ws_floats = wsf;
+  a->tflag_tiles = mt;
+  *ws_floats = (size_t)std::max(ws, 1ll) * 2;
+  *cnt_ints = std::max(cnt, 1);
   *max_tiles = mt;
 }
 
@@ -1037,7 +1135,7 @@ int forward_smem_bytes(int stages, int hd, int group) {
 
 template <int HD, int G, int MINB>
 static cudaError_t launch_m(const FwArgs& a, const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& m2,
-                            int grid, int stages, cudaStream_t st) {
+                            const CUtensorMap& m3, int grid, int stages, cudaStream_t st) {
   const int smem = forward_smem_bytes(stages, HD, G);
   static int attr = 0;
   if (smem > attr) {
@@ -1047,7 +1145,7 @@ static cudaError_t launch_m(const FwArgs& a, const CUtensorMap& m0, const CUtens
   }
   FwArgs b = a;
   b.stages = stages;
-  k_forward<HD, G, MINB><<<grid, kThreads, smem, st>>>(m0, m1, m2, b);
+  k_forward<HD, G, MINB><<<grid, kThreads, smem, st>>>(m0, m1, m2, m3, b);
   return cudaGetLastError();
 }
 
@@ -1055,17 +1153,17 @@ static cudaError_t launch_m(const FwArgs& a, const CUtensorMap& m0, const CUtens
 // take the register-capped instance so that two CTAs fit the register file too.
 template <int HD, int G>
 static cudaError_t launch_t(const FwArgs& a, const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& m2,
-                            int grid, int stages, cudaStream_t st) {
+                            const CUtensorMap& m3, int grid, int stages, cudaStream_t st) {
   if (forward_smem_bytes(stages, HD, G) <= 232448 / 2 - 1024)
-    return launch_m<HD, G, 2>(a, m0, m1, m2, grid, stages, st);
-  return launch_m<HD, G, 1>(a, m0, m1, m2, grid, stages, st);
+    return launch_m<HD, G, 2>(a, m0, m1, m2, m3, grid, stages, st);
+  return launch_m<HD, G, 1>(a, m0, m1, m2, m3, grid, stages, st);
 }
 
 cudaError_t launch_forward(const FwArgs& a, const CUtensorMap& m_xa, const CUtensorMap& m_attn,
-                           const CUtensorMap& m_act, int grid, int stages, cudaStream_t st) {
+                           const CUtensorMap& m_act, const CUtensorMap& m_xb, int grid, int stages, cudaStream_t st) {
   const int G = a.H / a.KV;
 #define AMUSD_FW(HD_, G_) \
-  if (a.hd == HD_ && G == G_) return launch_t<HD_, G_>(a, m_xa, m_attn, m_act, grid, stages, st);
+  if (a.hd == HD_ && G == G_) return launch_t<HD_, G_>(a, m_xa, m_attn, m_act, m_xb, grid, stages, st);
   AMUSD_FW(64, 2) AMUSD_FW(64, 4) AMUSD_FW(64, 8) AMUSD_FW(128, 2) AMUSD_FW(128, 4) AMUSD_FW(128, 8)
 #undef AMUSD_FW
   return cudaErrorInvalidValue;

@@ -30,8 +30,12 @@ struct GemmKind {
   __nv_bfloat16* out_b;         // GateUp output (bf16)
   __nv_bfloat16* xnext;         // Resid: next GEMM input bf16(h * gnext)
   const __nv_bfloat16* gnext;   // Resid: next RMSNorm weight, layer 0
+  float* ssp_in;                // RMSNorm sums of this GEMM's input rows (StoreScaled / GateUp / Argmax)
+  float* ssp_out;               // Resid: RMSNorm sums of the next GEMM's input
+  long long ws_off;             // this kind's int64 split-K accumulator region (elements into FwArgs::ws)
+  int cnt_off;                  // this kind's tile counters (ints into FwArgs::tile_cnt)
   int gnext_stride;             // elements between layers
-  int epi, map;                 // epilogue, X tensor map (0 xa [16][d], 1 attn [16][H*hd], 2 act [16][ffn])
+  int epi, map;                 // epilogue, X map (0 xa, 1 attn, 2 act, 3 xb)
   int ntiles, kb, kc, nchunks, nitems;  // 128-row tiles, 64-wide K units per tile, units per item, items per tile
   int N, ldo;
 };
@@ -46,9 +50,14 @@ struct FwArgs {
   const __nv_bfloat16* embed;
   const __nv_bfloat16* norms;   // packed RMSNorm weights [2L+1][d]: attn(l) at 2l, mlp(l) at 2l+1, final at 2L
   float* h;                     // [16][d] residual stream
-  __nv_bfloat16* xa;            // [16][d] bf16(h * g) input of QKV / gate-up / LM head
-  float* ssp;                   // [16][d/128] per-tile sum of squares of h
-  float* qkv;                   // [16][(H+2KV)hd]
+  __nv_bfloat16* xa;            // [16][d] bf16(h * g): input of QKV / LM head (written by embed / down)
+  float* ssp;                   // [16][d/128] per-tile sum of squares of h (pairs with xa)
+  __nv_bfloat16* xb;            // [16][d] input of gate-up (written by O): double buffer of xa
+  float* sspb;                  // pairs with xb
+  long long* tflag;             // per-tile completion stamps of QKV / O / GU / DOWN (one 128-byte line each)
+  int tflag_tiles;              // tiles per kind region
+  int* agrp;                    // [L][KV] attention items finished per head group (self-resetting)
+  float* qkv;                   // [16][(H+2KV)hd], group-blocked (qkv_group_row)
   __nv_bfloat16* attn_b;        // [16][H hd]
   char* kcache;                 // [L][KV][S][hd] bf16
   char* vcache;
@@ -69,6 +78,7 @@ struct FwArgs {
   size_t qo_bytes;              // QKV + O tiled weight bytes of one layer (contiguous)
   int inflight;                 // max unlanded weight units per CTA (0 = ring depth)
   int debug;                    // perf-isolation bits (AMUSD_FW_DEBUG), 0 in production
+  int fine;                     // 1: per-tile dependencies (AMUSD_FW_FINE); 0: phase-level (default)
   long long* dbg;               // optional per-item timeline [item][8] (perf analysis), null in production
   int dbg_items;
 };
@@ -89,12 +99,19 @@ struct ModelView {
   float* h;
   float* qkv;
   __nv_bfloat16* xa;
+  __nv_bfloat16* xb;
+  float* ssp;
+  float* sspb;
   __nv_bfloat16* act_b;
 };
-void build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_floats, int* max_tiles);
+// ws_floats: int64 accumulator regions of all kinds (in float units); cnt_ints: tile counters;
+// max_tiles: largest producer tile count (flag region size).
+void build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_floats, int* cnt_ints, int* max_tiles);
 
 cudaError_t launch_forward(const FwArgs& a, const CUtensorMap& m_xa, const CUtensorMap& m_attn,
-                           const CUtensorMap& m_act, int grid, int stages, cudaStream_t st);
+                           const CUtensorMap& m_act, const CUtensorMap& m_xb, int grid, int stages, cudaStream_t st);
+// schedule counters: grab, exit, epoch, then one per phase (kCounterInts each)
+inline size_t sched_ints(int L) { return (size_t)(3 + num_phases(L)) * kCounterInts; }
 int forward_smem_bytes(int stages, int hd, int group);
 
 }  // namespace fw

@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
 // Gate/up pair (src2 != null): tile t = gate rows 64t.. (lanes 0-63) then up
 // rows 64t.. (lanes 64-127), matching the fused SiLU*mul epilogue.
 __global__ void k_tile_weights(const __nv_bfloat16* __restrict__ src, const __nv_bfloat16* __restrict__ src2,
-                               __nv_bfloat16* __restrict__ dst, int N, int K) {
+                               __nv_bfloat16* __restrict__ dst, int N, int K, int qkv_H, int qkv_KV, int qkv_hd) {
   const int kb = K / BK;
   const size_t total = (size_t)(src2 ? 2 * N : N) * K;
   for (size_t o = blockIdx.x * (size_t)blockDim.x + threadIdx.x; o < total; o += (size_t)gridDim.x * blockDim.x) {
@@ -329,15 +329,19 @@ __global__ void k_tile_weights(const __nv_bfloat16* __restrict__ src, const __nv
     int n;
     if (src2) { n = t * (BM / 2) + (i & (BM / 2 - 1)); s = i < BM / 2 ? src : src2; }
     else { n = t * BM + i; s = src; }
+    if (qkv_H) {  // QKV rows in group blocks [q(G heads) | k | v] per KV head (qkv_group_row)
+      n = qkv_group_row(n, qkv_H, qkv_KV, qkv_hd);
+    }
     dst[o] = s[(size_t)n * K + k];
   }
 }
 
 size_t tiled_bytes(int N, int K) { return (size_t)N * K * 2; }
 
-cudaError_t launch_tile_weights(const void* src, const void* src2, void* dst, int N, int K, cudaStream_t st) {
+cudaError_t launch_tile_weights(const void* src, const void* src2, void* dst, int N, int K, cudaStream_t st,
+                               int qkv_H, int qkv_KV, int qkv_hd) {
   k_tile_weights<<<148 * 8, 256, 0, st>>>((const __nv_bfloat16*)src, (const __nv_bfloat16*)src2,
-                                          (__nv_bfloat16*)dst, N, K);
+                                          (__nv_bfloat16*)dst, N, K, qkv_H, qkv_KV, qkv_hd);
   return cudaGetLastError();
 }
 

@@ -42,7 +42,11 @@ bool make_map(CUtensorMap* m, const void* ptr, int rows, int cols, int box_rows)
 // Re-layout a row-major bf16 [N][K] matrix (or a gate/up pair) into the
 // tile-contiguous SW128 layout read by the GEMM (one 16 KB bulk copy per unit).
 size_t tiled_bytes(int N, int K);
-cudaError_t launch_tile_weights(const void* src, const void* src2, void* dst, int N, int K, cudaStream_t st);
+// qkv_H > 0: the QKV weight rows are re-ordered into per-KV-head group blocks
+// [q of the G heads | k | v] (qkv_group_row), so a head group's outputs are
+// produced by consecutive 128-row tiles.
+cudaError_t launch_tile_weights(const void* src, const void* src2, void* dst, int N, int K, cudaStream_t st,
+                                int qkv_H = 0, int qkv_KV = 0, int qkv_hd = 0);
 int tc_grid(int ntiles, int kb);
 cudaError_t launch_gemm_tc(const CUtensorMap& mx, const TcArgs& a, cudaStream_t st, bool pdl);
 cudaError_t launch_embed_tc(const StepCtl* ctl, const void* emb, float* h, const void* g, void* xb, float* ssp,

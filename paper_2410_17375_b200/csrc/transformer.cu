@@ -272,10 +272,14 @@ __global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
   if (split >= nsplit) return;
   const int lo = split * kAttnChunk, hi = min(p + 1, lo + kAttnChunk);
   const int half = HD / 2, ncols = (a.H + 2 * a.KV) * HD;
+  // column offsets of this group's q / k / v (natural [q|k|v] or group-blocked layout)
+  const int qoff = a.blocked ? g * (GROUP + 2) * HD : g * GROUP * HD;
+  const int koff = a.blocked ? qoff + GROUP * HD : (a.H + g) * HD;
+  const int voff = a.blocked ? qoff + (GROUP + 1) * HD : (a.H + a.KV + g) * HD;
   // rotated queries of the group
   for (int i = threadIdx.x; i < GROUP * half; i += blockDim.x) {
     const int j = i / half, e = i - j * half;
-    const float* q = a.qkv + (size_t)r * ncols + (g * GROUP + j) * HD;
+    const float* q = a.qkv + (size_t)r * ncols + qoff + j * HD;
     const float c = a.cos[(size_t)p * half + e], s = a.sin[(size_t)p * half + e];
     qs[j][e] = q[e] * c - q[e + half] * s;
     qs[j][e + half] = q[e + half] * c + q[e] * s;
@@ -285,14 +289,14 @@ __global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
   for (int i = threadIdx.x; i < (jmax + 1) * half; i += blockDim.x) {
     const int j = i / half, e = i - j * half;
     const int pj = pos0 + j;
-    const float* kr = a.qkv + (size_t)j * ncols + (a.H + g) * HD;
+    const float* kr = a.qkv + (size_t)j * ncols + koff;
     const float c = a.cos[(size_t)pj * half + e], s = a.sin[(size_t)pj * half + e];
     kn[j][e] = Elem<WT>::to_f(Elem<WT>::from_f(kr[e] * c - kr[e + half] * s));
     kn[j][e + half] = Elem<WT>::to_f(Elem<WT>::from_f(kr[e + half] * c + kr[e] * s));
   }
   for (int i = threadIdx.x; i < (jmax + 1) * HD; i += blockDim.x) {
     const int j = i / HD, e = i - j * HD;
-    vn[j][e] = Elem<WT>::to_f(Elem<WT>::from_f(a.qkv[(size_t)j * ncols + (a.H + a.KV + g) * HD + e]));
+    vn[j][e] = Elem<WT>::to_f(Elem<WT>::from_f(a.qkv[(size_t)j * ncols + voff + e]));
   }
   __syncthreads();
   WT* kc = (WT*)a.kc + (size_t)g * a.S * HD;

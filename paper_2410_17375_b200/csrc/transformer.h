@@ -39,6 +39,7 @@ struct AttnArgs {
   float* ws;               // split partials [KV][KMAX][max_splits][group][hd+2]
   int* counters;           // [KV][KMAX] arrival counters (self re-arming)
   int max_splits;
+  int blocked;             // qkv in group-blocked layout (tensor-core models, qkv_group_row)
 };
 
 int attn_max_splits(int max_seq);
