@@ -741,7 +741,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
               continue;
             }
             mbar_expect_tx(smem_u32(&wfull[s]), kWBytes);
-            bulk_load(smem_u32(sW + s * kWBytes), src + (size_t)u * kWBytes, kWBytes, smem_u32(&wfull[s]), pol_w);
+            if (a.debug & 16)  // perf knob: no L2 eviction hint on the weight stream
+              bulk_load_nohint(smem_u32(sW + s * kWBytes), src + (size_t)u * kWBytes, kWBytes, smem_u32(&wfull[s]));
+            else
+              bulk_load(smem_u32(sW + s * kWBytes), src + (size_t)u * kWBytes, kWBytes, smem_u32(&wfull[s]), pol_w);
           }
           dbg_mark(a, i, 2, globaltimer());
         }

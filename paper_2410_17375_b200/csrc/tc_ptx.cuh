@@ -58,6 +58,12 @@ AMUSD_DEV void bulk_load(uint32_t dst, const void* src, int bytes, uint32_t mbar
       "l"(src), "r"(bytes), "r"(mbar), "l"(policy)
       : "memory");
 }
+// Same copy without an L2 cache hint.
+AMUSD_DEV void bulk_load_nohint(uint32_t dst, const void* src, int bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
 AMUSD_DEV uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
