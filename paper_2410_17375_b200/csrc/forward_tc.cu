@@ -241,7 +241,7 @@ struct EpiSmem {
 // 16 token rows.  Activations written here are read by other CTAs of the same
 // launch: all loads/stores bypass L1 (.cg).
 AMUSD_DEV void tile_epilogue(const FwArgs& a, const GemmKind& ph, const __nv_bfloat16* gnext, int t, int nl,
-                             const float* v, int rows, EpiSmem* es, int q, int lane) {
+                             const float* v, int rows, EpiSmem* es, int q, int lane, const float* hpre = nullptr) {
   const float* inv = es->inv;
   if (ph.epi == kEpStoreScaled) {
     const int n = t * BM + nl;
@@ -255,7 +255,7 @@ AMUSD_DEV void tile_epilogue(const FwArgs& a, const GemmKind& ph, const __nv_bfl
     for (int r = 0; r < BN; ++r) {
       float hn = 0.f;
       if (r < rows) {
-        hn = __ldcg(ph.out + (size_t)r * ph.ldo + n) + v[r];
+        hn = (hpre ? hpre[r] : __ldcg(ph.out + (size_t)r * ph.ldo + n)) + v[r];
         __stcg(ph.out + (size_t)r * ph.ldo + n, hn);
         ph.xnext[(size_t)r * ph.ldo + n] = __float2bfloat16(hn * gn);
       }
@@ -564,14 +564,17 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
     __stcg(ws + tid * (HD + 2) + HD + 1, sm->stat[1][tid]);
   }
   named_bar(1, 128);
+  // The row's last split (grabbed after its other splits) merges; the others publish and go.
+  int* cnt = a.attn_cnt + (g * KMAX + r) * kPad;
+  if (split != nsplit - 1) {
+    if (tid == 0) red_add_release(cnt, 1);
+    return;
+  }
   if (tid == 0) {
-    int* cnt = a.attn_cnt + (g * KMAX + r) * kPad;
-    const int old = atom_add_acq_rel(cnt, 1);
-    sm->last = (old == nsplit - 1);
-    if (sm->last) *cnt = 0;
+    wait_count(cnt, nsplit - 1);
+    *cnt = 0;
   }
   named_bar(1, 128);
-  if (!sm->last) return;
   const float* base = a.attn_ws + ((size_t)g * KMAX + r) * a.max_splits * G * (HD + 2);
   for (int i = tid; i < G * HD; i += 128) {
     const int j = i / HD, e = i - j * HD;
@@ -917,7 +920,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
         // chunks it waits for.
         const int cj = j / g.ntiles, t = j - cj * g.ntiles;
         bool final = true;
-        float acc[BN];
+        float acc[BN], hpre[BN];
+        bool have_hpre = false;
         if (nchunks > 1) {
           // Split-K in exact int64 fixed point (2^-32): the red.adds commute, so the merged
           // tile is bit-identical whatever the chunks' arrival order (deterministic, batch
@@ -935,9 +939,17 @@ __global__ void __launch_bounds__(kThreads, MINB)
           if (!final) {
             if (tid == 0) red_add_release(a.tile_cnt + g.cnt_off + t * kPad, 1);
           } else {
+            // residual rows do not depend on this phase: load them while waiting for the chunks
+            if (epi == kEpResid) {
+#pragma unroll
+              for (int r = 0; r < BN; ++r)
+                hpre[r] = r < L.rows ? __ldcg(g.out + (size_t)r * g.ldo + t * BM + nl) : 0.f;
+              have_hpre = true;
+            }
             if (tid == 0) {
               wait_count(a.tile_cnt + g.cnt_off + t * kPad, nchunks - 1);
               a.tile_cnt[g.cnt_off + t * kPad] = 0;  // re-arm for the next phase / launch
+              if (a.dbg) dbg_mark(a, phase_first(a, L, p) + j, 6, globaltimer());
             }
             named_bar(1, 128);
             long long s64[BN];
@@ -955,7 +967,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         }
         if (final) {
           const __nv_bfloat16* gnext = g.gnext ? g.gnext + (size_t)layer * g.gnext_stride : nullptr;
-          tile_epilogue(a, g, gnext, t, nl, acc, L.rows, es, q, lane);
+          tile_epilogue(a, g, gnext, t, nl, acc, L.rows, es, q, lane, have_hpre ? hpre : nullptr);
         }
         wrote = final;
         lm_last_check = epi == kEpArgmax;
@@ -996,6 +1008,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
       }
       // publish: this item's writes are visible (generic and async proxy) before the count
       // (CTA barrier, then one release by thread 0: the cooperative-groups grid-sync pattern).
+      if (a.dbg && tid == 0) dbg_mark(a, phase_first(a, L, p) + j, 7, globaltimer());
       if (wrote) fence_proxy_async();
       named_bar(1, 128);
       if (tid == 0) {

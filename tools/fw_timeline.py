@@ -1,7 +1,7 @@
 """Record the per-item timeline of one persistent forward (perf analysis).
 
   python tools/fw_timeline.py [--model 8b] [--layers 8] [--rows 1] --out gpurun_out/tl.npy
-Columns: item, cta, phase, t_grab, t_issued, t_dep, t_mma, t_done (ns, globaltimer).
+Columns: item, cta, phase, t_grab, t_issued, t_dep, t_mma, t_done, t_waited, t_epi_done (ns, globaltimer).
 """
 import argparse
 import ctypes as C
@@ -39,10 +39,11 @@ torch.cuda.synchronize()
 t = buf.cpu().numpy()
 n = int((t[:, 1] != 0).sum())
 t = t[:n]
-out = np.zeros((n, 8), dtype=np.int64)
+out = np.zeros((n, 10), dtype=np.int64)
 out[:, 0] = t[:, 0] & 0xFFFFF
 out[:, 1] = (t[:, 0] >> 20) & 0xFFF
 out[:, 2] = t[:, 0] >> 32
 out[:, 3:8] = t[:, 1:6]
+out[:, 8:10] = t[:, 6:8]  # merger: count-wait done, final epilogue done (before publish)
 np.save(a.out, out)
 print(f"{n} items, forward {ms.value:.4f} ms (timed with the timeline on)")
