@@ -937,7 +937,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
           // with a fire-and-forget release and move on -- no round trip in their epilogue.
           final = cj == nchunks - 1;
           if (!final) {
-            if (tid == 0) red_add_release(a.tile_cnt + g.cnt_off + t * kPad, 1);
+            if (tid == 0) {
+              if (a.debug & 32) red_add_relaxed(a.tile_cnt + g.cnt_off + t * kPad, 1);  // timing experiment only
+              else red_add_release(a.tile_cnt + g.cnt_off + t * kPad, 1);
+            }
           } else {
             // residual rows do not depend on this phase: load them while waiting for the chunks
             if (epi == kEpResid) {

@@ -32,6 +32,7 @@ CLOCK_VIRTUAL = "virtual"
 CLOCK_DEVICE = "wall"  # %globaltimer is a wall clock (ns); reported as "wall"
 
 TRACE_CSV_COLUMNS = ["t_ms", "actor", "kind", "pos_lo", "pos_hi", "busy_ms", "draft_accepted"]
+TIMELINE_CSV_COLUMNS = ["t_ms", "verified_tokens"]  # metrics.py:57
 
 # device event kind codes (include/amusd.h amusd_trace_event)
 _DEVICE_KINDS = {0: DRAFT_TOKEN, 1: VERIFY_ACCEPT, 2: VERIFY_CORRECT, 3: ROLLBACK}
@@ -218,3 +219,52 @@ def overlap_ms(a: list, b: list) -> float:
         else:
             j += 1
     return total
+
+
+def read_trace_csv(path, clock: str, prompt_length: int) -> DecodeTrace:
+    """Rebuild a trace from an event CSV written by ``trace_to_csv`` (metrics.py:358-374)."""
+    events = []
+    with open(path, newline="", encoding="utf-8") as fh:
+        rows = csv.reader(fh)
+        if next(rows, None) != TRACE_CSV_COLUMNS:
+            raise InvalidInputError(f"unexpected trace CSV header in {path}")
+        for t_ms, actor, kind, lo, hi, busy, acc in rows:
+            events.append(TraceEvent(float(t_ms), actor, kind, int(lo), int(hi), float(busy), int(acc)))
+    return DecodeTrace(clock=clock, prompt_length=prompt_length, events=events)
+
+
+def export_timeline(trace: DecodeTrace) -> list:
+    """Cumulative verified tokens over time, capped at the generated count (metrics.py:282-298)."""
+    trace.validate()
+    cap = trace.events[-1].pos_hi - trace.prompt_length
+    series, done = [(0.0, 0)], 0
+    for e in trace.events:
+        if e.kind in VERIFY_KINDS:
+            done = min(done + e.token_count, cap)
+            series.append((e.t_ms, done))
+    return series
+
+
+def timeline_to_csv(series) -> str:
+    buf = io.StringIO()
+    w = csv.writer(buf, lineterminator="\n")
+    w.writerow(TIMELINE_CSV_COLUMNS)
+    for t_ms, n in series:
+        w.writerow([repr(t_ms), n])
+    return buf.getvalue()
+
+
+def compare_table(entries) -> dict:
+    """Speedup of each (label, mean_ms_per_token) over the first (metrics.py:264-276)."""
+    if len(entries) < 2:
+        raise InvalidInputError("a comparison needs at least two entries")
+    base = entries[0][1]
+    return {"baseline": entries[0][0],
+            "rows": [{"label": k, "mean_ms_per_token": v, "speedup": base / v} for k, v in entries]}
+
+
+def compare_text(table: dict) -> str:
+    width = max(len("strategy"), *(len(r["label"]) for r in table["rows"]))
+    out = [f"{'strategy':<{width}}  {'mean ms/token':>14}  {'speedup':>8}"]
+    out += [f"{r['label']:<{width}}  {r['mean_ms_per_token']:>14.3f}  {r['speedup']:>7.2f}x" for r in table["rows"]]
+    return "\n".join(out)

@@ -21,7 +21,7 @@ ap.add_argument("--pos", type=int, default=300)
 ap.add_argument("--path", default="persistent")
 a = ap.parse_args()
 TC = P.TransformerConfig
-kw = {"max_seq": 640}
+kw = {"max_seq": max(640, a.pos + 64)}
 if a.layers:
     kw["n_layers"] = a.layers
 cfg = TC.llama_8b(**kw) if a.model == "8b" else TC.llama_1b(**kw)
