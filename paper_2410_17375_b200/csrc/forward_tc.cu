@@ -578,14 +578,33 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
   const float* base = a.attn_ws + ((size_t)g * KMAX + r) * a.max_splits * G * (HD + 2);
   for (int i = tid; i < G * HD; i += 128) {
     const int j = i / HD, e = i - j * HD;
-    float M = -INFINITY;
-    for (int s2 = 0; s2 < nsplit; ++s2) M = fmaxf(M, __ldcg(base + ((size_t)s2 * G + j) * (HD + 2) + HD));
-    float Ls = 0.f, O = 0.f;
-    for (int s2 = 0; s2 < nsplit; ++s2) {
-      const float* w = base + ((size_t)s2 * G + j) * (HD + 2);
-      const float f = expf(__ldcg(w + HD) - M);
-      Ls += __ldcg(w + HD + 1) * f;
-      O += __ldcg(w + e) * f;
+    // splits in batches of 8 with every load of a batch in flight, merged in split order
+    float M = -INFINITY, Ls = 0.f, O = 0.f;
+    for (int b0 = 0; b0 < nsplit; b0 += 8) {
+      float m[8], l[8], o[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float* w = base + ((size_t)(b0 + u) * G + j) * (HD + 2);
+        const bool ok = b0 + u < nsplit;
+        m[u] = ok ? __ldcg(w + HD) : -INFINITY;
+        l[u] = ok ? __ldcg(w + HD + 1) : 0.f;
+        o[u] = ok ? __ldcg(w + e) : 0.f;
+      }
+      float Mb = M;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) Mb = fmaxf(Mb, m[u]);
+      const float f0 = M == -INFINITY ? 0.f : expf(M - Mb);  // rescale the running sums
+      Ls *= f0;
+      O *= f0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (b0 + u < nsplit) {
+          const float f = expf(m[u] - Mb);
+          Ls += l[u] * f;
+          O += o[u] * f;
+        }
+      }
+      M = Mb;
     }
     out[(size_t)r * ldo + (g * G + j) * HD + e] = __float2bfloat16(O / Ls);
   }
@@ -906,7 +925,16 @@ __global__ void __launch_bounds__(kThreads, MINB)
           const float* ssp_in = g.ssp_in;
           const int nt = a.d / BM, rr = tid >> 3, part = tid & 7;
           float tot = 0.f;
-          for (int k = part; k < nt; k += 8) tot += __ldcg(ssp_in + (size_t)rr * nt + k);
+          {  // all loads first (one round trip), then the fixed-order sum; d <= 8192 -> <= 8 per thread
+            float vals[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int k = part + 8 * u;
+              vals[u] = k < nt ? __ldcg(ssp_in + (size_t)rr * nt + k) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) tot += vals[u];
+          }
           tot += __shfl_xor_sync(0xffffffffu, tot, 1);
           tot += __shfl_xor_sync(0xffffffffu, tot, 2);
           tot += __shfl_xor_sync(0xffffffffu, tot, 4);
@@ -1096,8 +1124,11 @@ void build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_f
                   const char* name) {
     GemmKind g{};
     g.epi = epi; g.map = map; g.ntiles = ntiles; g.kb = K / BK;
+    // QKV / O sit on the latency-bound part of the layer chain: half-size items; the LM head
+    // takes whole-K items (no split-K merge before the argmax) -- both measured best
     const bool chain = name[0] == 'Q' || (name[0] == 'O' && name[1] == 0);
-    g.kc = pick_kc(g.kb, kind_units(name, chain ? std::max(1, units_per_item / 2) : units_per_item));
+    const bool lm = name[0] == 'L';
+    g.kc = pick_kc(g.kb, kind_units(name, chain ? std::max(1, units_per_item / 2) : (lm ? 64 : units_per_item)));
     g.nchunks = g.kb / g.kc;
     g.nitems = ntiles * g.nchunks;
     g.N = N; g.ldo = ldo; g.wt = wt; g.wt_stride = stride;
