@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--profile-only", action="store_true", help="one AMUSD decode, no extras (for ncu)")
     ap.add_argument("--engines", default="ar,sync,amusd", help="subset of ar,sync,amusd to time")
     ap.add_argument("--no-extras", action="store_true", help="skip roofline/e2e/cpu legs (quick sweeps)")
+    ap.add_argument("--layout", default="replicas", choices=["replicas", "split"],
+                    help="N>1: independent co-located pairs per GPU (default), or (N=2) the paper's split pair: "
+                         "draft on rank 0's GPU, verify on rank 1's (BASELINE config 2)")
     return ap.parse_args()
 
 
@@ -109,6 +112,49 @@ class ClockSampler:
         reasons = sorted({n for r in rows for n, v in zip(names, r[3:7]) if v.lower().startswith("active")})
         return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(float(r[1]) for r in rows),
                 "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------- split pair (config 2)
+def split_arm(args, rank: int, world: int, local_rank: int):
+    """BASELINE config 2: draft on GPU0 (rank 0), verify on GPU1 (rank 1), P2P mailbox."""
+    import torch
+    import paper_2410_17375_b200 as P
+    from paper_2410_17375_b200.split import SplitLink, decode_speculative_async_split
+    if world != 2:
+        raise SystemExit("--layout split needs exactly 2 ranks")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    TC = P.TransformerConfig
+    N, Plen = args.new_tokens, args.prompt_len
+    max_seq = Plen + N + 64
+    link = SplitLink()
+    if link.role == "draft":
+        model = P.AgreementDraft(P.TransformerModel(TC.llama_1b(max_seq=max_seq), seed=1, device=dev), args.rho,
+                                 coin_seed=1234)
+    else:
+        model = P.TransformerModel(TC.llama_8b(max_seq=max_seq), seed=0, device=dev)
+    prompt = synthetic_prompt(Plen, 128256)
+    cfg = P.DecodeConfig(max_new_tokens=N, draft_window_k=args.k, max_draft_lead=args.lead or None)
+    for _ in range(args.warmup):
+        decode_speculative_async_split(model, prompt, cfg, link=link, max_window=args.window)
+    total, toks = 0.0, 0
+    for _ in range(args.steps):
+        res, (dms, vms) = decode_speculative_async_split(model, prompt, cfg, link=link, max_window=args.window)
+        total += max(dms, vms)      # device-timed, max over the two GPUs
+        toks += len(res.tokens)
+    if rank == 0:
+        v = toks / (total / 1000.0)
+        print(json.dumps({
+            "metric": METRIC, "value": round(v, 2), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(total / args.steps, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init weights, seeded prompt)",
+            "config": {"workload": "cfg2: Llama-3.2-1B-shaped draft on GPU0 + Llama-3.1-8B-shaped verify on GPU1, "
+                                   "P2P mailbox over NVLink", "rho": args.rho, "new_tokens": N, "prompt_len": Plen,
+                       "parallelism": "split pair (draft | verify)"},
+            "amusd": {"tokens_per_s": round(v, 3), "verify_steps": res.stats.verify_steps,
+                      "rollbacks": res.stats.rollbacks, "drafted": res.stats.drafted_tokens},
+            "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": None, "clocks": None}))
 
 
 # --------------------------------------------------------------- GPU arm
@@ -351,6 +397,8 @@ def main():
         torch.distributed.init_process_group("nccl" if args.impl == "amusd" else "gloo")
     if args.impl == "reference":
         reference_arm(args, rank, world)
+    elif args.layout == "split":
+        split_arm(args, rank, world, local_rank)
     else:
         out = gpu_arm(args, rank, world, local_rank)
         if out is None:

@@ -164,6 +164,10 @@ int amusd_session_reset(amusd_session* s, const int32_t* prompt, int n, void* st
 /* Launch one engine as device-driven CUDA graphs (conditional WHILE loops):
  * no host sync inside; returns after enqueueing. ASYNC uses both streams. */
 int amusd_session_launch(amusd_session* s, int engine, void* verify_stream, void* draft_stream);
+/* Capture + instantiate an engine's graphs without launching (launch does it on
+ * first use).  A split pair builds both halves first: instantiation may wait
+ * for the device, which must not happen while the peer's loop is spinning. */
+int amusd_session_build(amusd_session* s, int engine);
 
 /* Verified stream V and counters after a run (host buffers). */
 typedef struct {
@@ -198,6 +202,18 @@ int amusd_session_kernels_per_step(amusd_session* s, int engine, int* draft_step
 /* Device-side deterministic weight fill: w[i] = scale * u(splitmix64(seed + i)),
  * u uniform in [-1,1) -- used for synthetic bf16/fp32 weights. */
 int amusd_fill_uniform(void* dst, int dtype, size_t n, uint64_t seed, float scale, void* stream);
+
+/* ---------------------------------------------- split pair (2 GPUs) */
+/* The draft GPU and the verify GPU each own a mailbox copy and store into the
+ * peer's copy over NVLink (coordination.py:114-275 across a device boundary).
+ * Export a device buffer as a CUDA IPC handle (64 bytes) plus its offset in
+ * the underlying allocation; import maps the peer's buffer into this process
+ * (peer access enabled lazily).  amusd_ipc_close unmaps an imported base. */
+int amusd_ipc_export(void* ptr, uint8_t handle[64], size_t* offset);
+int amusd_ipc_import(const uint8_t handle[64], size_t offset, void** ptr, void** base);
+int amusd_ipc_close(void* base);
+/* %globaltimer of this device (ns), for aligning the two GPUs' trace clocks. */
+int amusd_device_clock(int64_t* ns, void* stream);
 
 #ifdef __cplusplus
 }

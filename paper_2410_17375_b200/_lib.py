@@ -84,11 +84,16 @@ SIGNATURES = [
     ("amusd_session_destroy", _I, [_VP]),
     ("amusd_session_reset", _I, [_VP, _P(C.c_int32), _I, _VP]),
     ("amusd_session_launch", _I, [_VP, _I, _VP, _VP]),
+    ("amusd_session_build", _I, [_VP, _I]),
     ("amusd_session_info", _I, [_VP, _P(RunInfo), _P(C.c_int32), _I, _VP]),
     ("amusd_session_trace", _I, [_VP, _I, _P(TraceEvent), _I, _P(_I), _VP]),
     ("amusd_time_forward", _I, [_VP, _I, _I, _I, _I, _P(C.c_float), _VP]),
     ("amusd_session_kernels_per_step", _I, [_VP, _I, _P(_I), _P(_I)]),
     ("amusd_fill_uniform", _I, [_VP, _I, _SZ, C.c_uint64, C.c_float, _VP]),
+    ("amusd_ipc_export", _I, [_VP, _P(C.c_uint8), _P(_SZ)]),
+    ("amusd_ipc_import", _I, [_P(C.c_uint8), _SZ, _P(_VP), _P(_VP)]),
+    ("amusd_ipc_close", _I, [_VP]),
+    ("amusd_device_clock", _I, [_P(C.c_int64), _VP]),
 ]
 
 _lib = None

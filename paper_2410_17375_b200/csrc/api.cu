@@ -1013,6 +1013,23 @@ static int build_loop(amusd_session* s, int engine, int actor, cudaGraphExec_t* 
 
 extern "C" {
 
+// Build (capture + instantiate) the engine's graphs without launching them.
+int amusd_session_build(amusd_session* s, int engine) {
+  if (!s) return fail(AMUSD_ERR_INVALID_INPUT, "null session");
+  if (engine < 0 || engine > AMUSD_ENGINE_ASYNC_VERIFY) return fail(AMUSD_ERR_INVALID_INPUT, "unknown engine");
+  const bool need_d = engine != AMUSD_ENGINE_AUTOREGRESSIVE && engine != AMUSD_ENGINE_ASYNC_VERIFY;
+  const bool need_v = engine != AMUSD_ENGINE_ASYNC_DRAFT;
+  if (need_d && !s->draft) return fail(AMUSD_ERR_INVALID_INPUT, "engine needs a draft model");
+  if (need_v && !s->verify) return fail(AMUSD_ERR_INVALID_INPUT, "engine needs a verify model");
+  const int actors[2] = {need_d && engine != AMUSD_ENGINE_AUTOREGRESSIVE && engine != AMUSD_ENGINE_SYNC,
+                         need_v || engine == AMUSD_ENGINE_SYNC};
+  for (int actor = 0; actor < 2; ++actor)
+    if (actors[actor] && !s->exec[engine][actor])
+      if (int r = build_loop(s, engine, actor, &s->exec[engine][actor])) return r;
+  CUDA_TRY(cudaDeviceSynchronize());
+  return AMUSD_OK;
+}
+
 int amusd_session_launch(amusd_session* s, int engine, void* verify_stream, void* draft_stream) {
   if (!s) return fail(AMUSD_ERR_INVALID_INPUT, "null session");
   if (engine < 0 || engine > AMUSD_ENGINE_ASYNC_VERIFY) return fail(AMUSD_ERR_INVALID_INPUT, "unknown engine");
@@ -1138,5 +1155,63 @@ extern "C" int amusd_fill_uniform(void* dst, int dtype, size_t n, uint64_t seed,
   if (!dst) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
   k_fill_uniform<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(dst, dtype, n, seed, scale);
   CUDA_TRY(cudaGetLastError());
+  return AMUSD_OK;
+}
+
+// ------------------------------------------------------------ split pair
+extern "C" {
+
+int amusd_ipc_export(void* ptr, uint8_t handle[64], size_t* offset) {
+  if (!ptr || !handle || !offset) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  static PFN_cuMemGetAddressRange_v3020 range = nullptr;
+  if (!range) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(AMUSD_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    range = (PFN_cuMemGetAddressRange_v3020)p;
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS) return fail(AMUSD_ERR_CUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, (void*)base));
+  memcpy(handle, &h, 64);
+  *offset = (size_t)((CUdeviceptr)ptr - base);
+  return AMUSD_OK;
+}
+
+int amusd_ipc_import(const uint8_t handle[64], size_t offset, void** ptr, void** base) {
+  if (!handle || !ptr || !base) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, 64);
+  void* b = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&b, h, cudaIpcMemLazyEnablePeerAccess));
+  *base = b;
+  *ptr = (char*)b + offset;
+  return AMUSD_OK;
+}
+
+int amusd_ipc_close(void* base) {
+  if (!base) return AMUSD_OK;
+  CUDA_TRY(cudaIpcCloseMemHandle(base));
+  return AMUSD_OK;
+}
+
+}  // extern "C"
+
+__global__ void k_device_clock(long long* out) { *out = globaltimer(); }
+
+extern "C" int amusd_device_clock(int64_t* ns, void* stream) {
+  if (!ns) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  long long* d = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&d, sizeof(long long), (cudaStream_t)stream));
+  k_device_clock<<<1, 1, 0, (cudaStream_t)stream>>>(d);
+  long long v = 0;
+  CUDA_TRY(cudaMemcpyAsync(&v, d, sizeof(v), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  CUDA_TRY(cudaFreeAsync(d, (cudaStream_t)stream));
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  *ns = v;
   return AMUSD_OK;
 }
