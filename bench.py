@@ -122,6 +122,7 @@ def split_arm(args, rank: int, world: int, local_rank: int):
     from paper_2410_17375_b200.split import SplitLink, decode_speculative_async_split
     if world != 2:
         raise SystemExit("--layout split needs exactly 2 ranks")
+    local_rank %= torch.cuda.device_count()   # 2 ranks on 1 GPU: functional check of the same path
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     TC = P.TransformerConfig
@@ -393,8 +394,10 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if world > 1:
         import torch
-        torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl" if args.impl == "amusd" else "gloo")
+        if args.layout != "split":
+            torch.cuda.set_device(local_rank)
+        # the split pair's link is object collectives only (gloo); replicas time with NCCL
+        torch.distributed.init_process_group("nccl" if args.impl == "amusd" and args.layout != "split" else "gloo")
     if args.impl == "reference":
         reference_arm(args, rank, world)
     elif args.layout == "split":

@@ -113,6 +113,13 @@ def _result(verified, draft_rows, verify_rows, prompt_len, eos, config) -> Decod
     return DecodeResult(tokens, finished_by, summarize(trace), trace)
 
 
+def _mark_stale(session: DeviceSession) -> None:
+    """The loop advances the models' device state: the next run must init_state again."""
+    for m in (session.draft, session.verify):
+        if m is not None:
+            _model_of(m)._fresh = None
+
+
 def _run_halves(halves, prompt) -> list:
     """Reset both mailbox copies, then launch both loops with no cross-stream waits
     (the verify loop spins on the draft's tokens: a stream dependency would deadlock)."""
@@ -133,6 +140,7 @@ def _run_halves(halves, prompt) -> list:
             L.check(lib.amusd_session_launch(h.session._h, h.engine, h.stream.cuda_stream, h.stream.cuda_stream))
             end.record(h.stream)
             events.append((start, end))
+        _mark_stale(h.session)
     outs = []
     for h, (start, end) in zip(halves, events):
         with torch.cuda.device(h.session.device):
@@ -247,6 +255,7 @@ def decode_speculative_async_split(model, prompt: Sequence[int], config: DecodeC
             start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             start.record(st)
             L.check(lib.amusd_session_launch(s._h, half.engine, st.cuda_stream, st.cuda_stream))
+            _mark_stale(s)
             end.record(st)
             st.synchronize()
         ms = start.elapsed_time(end)

@@ -99,3 +99,22 @@ def test_split_pair_emulated_transformer():
     assert res.tokens == ar.tokens
     res.trace.validate()
     P.engines.clear_sessions()
+
+
+@pytest.mark.gpu
+def test_split_pair_two_processes_ipc():
+    """The distributed path proper: two processes, mailbox copies exchanged as CUDA IPC
+    handles (both on one GPU here; on two GPUs the peer stores go over NVLink)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, str(root / "tools" / "split_check.py"), "48"], capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-3000:]
+    out = {d["role"]: d for d in (json.loads(l) for l in r.stdout.splitlines() if l.startswith("{"))}
+    assert out["draft"]["tokens"] == out["verify"]["tokens"] == out["verify"]["ar"] == out["draft"]["ar"]
+    assert out["draft"]["rollbacks"] == out["verify"]["rollbacks"]
