@@ -111,6 +111,9 @@ int amusd_model_destroy(amusd_model* m);
  * Applies to launches enqueued afterwards (sessions capture it per engine). */
 enum { AMUSD_PATH_PERSISTENT = 0, AMUSD_PATH_KERNELS = 1, AMUSD_PATH_SIMT = 2 };
 int amusd_model_set_path(amusd_model* m, int path);
+/* Perf analysis only: run amusd_time_forward's persistent launches on `sms`
+ * SMs (0 = all), e.g. the share a co-located session gives the model. */
+int amusd_model_set_grid(amusd_model* m, int sms);
 /* Perf analysis only: record a per-work-item timeline of the persistent
  * forward into a device buffer (64 bytes per item; NULL disables). */
 int amusd_model_set_timeline(amusd_model* m, void* buf, size_t bytes);

@@ -69,6 +69,7 @@ SIGNATURES = [
     ("amusd_hash_create", _I, [_P(_VP), C.c_uint64, _I, _I, _I, C.c_double, _I, _VP, _SZ]),
     ("amusd_model_destroy", _I, [_VP]),
     ("amusd_model_set_path", _I, [_VP, _I]),
+    ("amusd_model_set_grid", _I, [_VP, _I]),
     ("amusd_model_set_timeline", _I, [_VP, _VP, _SZ]),
     ("amusd_init_state", _I, [_VP, _P(C.c_int32), _I, _VP]),
     ("amusd_next_token", _I, [_VP, _P(C.c_int32), _VP]),

@@ -113,6 +113,7 @@ struct amusd_model {
   float* fw_ws = nullptr;
   int* fw_tile_cnt = nullptr;
   int fw_grid = 0, fw_stages = 0;  // launch shape (set per engine at graph capture)
+  int grid_override = 0;            // amusd_model_set_grid: SMs of amusd_time_forward launches (0 = all)
   int path = AMUSD_PATH_PERSISTENT;
   long long* fw_dbg = nullptr;  // optional per-item timeline (amusd_model_set_timeline)
   int fw_dbg_items = 0;
@@ -594,6 +595,13 @@ int amusd_model_set_path(amusd_model* m, int path) {
   return AMUSD_OK;
 }
 
+int amusd_model_set_grid(amusd_model* m, int sms) {
+  if (!m) return fail(AMUSD_ERR_INVALID_INPUT, "null model");
+  if (sms < 0 || sms > num_sms()) return fail(AMUSD_ERR_INVALID_INPUT, "sms out of range");
+  m->grid_override = sms;
+  return AMUSD_OK;
+}
+
 }  // extern "C"
 
 // ------------------------------------------------- MockModel parity path
@@ -955,7 +963,7 @@ static int capture_body(amusd_session* s, int engine, int actor, cudaGraph_t bod
   // Co-located AMUSD: the draft and the verify forward run at the same time on DISJOINT SM
   // sets (each persistent CTA fills an SM; grids summing to <= #SMs can always co-run, and
   // the work-queue kernel needs no particular grid size).  Other engines own the GPU.
-  const int draft_sms = std::max(1, std::min(num_sms() - 1, env_int("AMUSD_FW_DRAFT_GRID", 56)));
+  const int draft_sms = std::max(1, std::min(num_sms() - 1, env_int("AMUSD_FW_DRAFT_GRID", 64)));
   for (amusd_model* m : {s->draft, s->verify}) {
     if (!m || !use_fw(m)) continue;
     m->fw_stages = env_int("AMUSD_FW_STAGES", fw_max_stages(m->cfg, 1));
@@ -1113,6 +1121,9 @@ int amusd_time_forward(amusd_model* m, int rows, int which, int layer, int iters
     if (use_tc(m, nr)) return tc_kernel(m, m->api_ctl, layer, which, st, false);
     return tf_kernel(m, m->api_ctl, nr, layer, which, st, false, false);
   };
+  const int grid0 = m->fw_grid;
+  if (m->grid_override > 0) m->fw_grid = m->grid_override;
+  struct Restore { amusd_model* m; int g; ~Restore() { m->fw_grid = g; } } restore{m, grid0};
   if (int r = once()) return r;  // warm-up
   cudaEvent_t e0, e1;
   CUDA_TRY(cudaEventCreate(&e0));

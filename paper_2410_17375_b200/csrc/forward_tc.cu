@@ -58,6 +58,7 @@ constexpr long long kWaitNs = 4ll * 1000 * 1000 * 1000;  // dependency waits tra
 // per phase, one per split-K tile): 148 CTAs poll and bump them concurrently.
 constexpr int kPad = kCounterInts;
 constexpr unsigned a_poll_ns = 100;
+constexpr unsigned kSuspendNs = 20000;  // mbarrier try_wait suspend-time hint
 
 // ------------------------------------------------------------ memory model
 AMUSD_DEV int ld_acquire_gpu(const int* p) {
@@ -104,15 +105,17 @@ AMUSD_DEV void mbar_wait_t(uint32_t addr, uint32_t parity) {
   if (ok) return;
   const long long t0 = globaltimer();
   for (int it = 0;; ++it) {
+    // suspend-time hint: the waiting warp sleeps (wakes as soon as the phase completes)
+    // instead of re-issuing, leaving the SMSP's issue slots to the epilogue warp
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(addr), "r"(parity)
+        : "r"(addr), "r"(parity), "r"(kSuspendNs)
         : "memory");
     if (ok) return;
-    if ((it & 255) == 255 && globaltimer() - t0 > kWaitNs) __trap();
+    if ((it & 15) == 15 && globaltimer() - t0 > kWaitNs) __trap();
   }
 }
 
@@ -197,14 +200,17 @@ AMUSD_DEV int2 locate(const FwArgs& a, const Lay& L, int i) {
   const int l = r / L.PL;
   if (l >= a.L) return make_int2(1 + 5 * a.L, r - a.L * L.PL);
   r -= l * L.PL;
-  int k = 4;
-  while (r < L.pre[k]) --k;
-  return make_int2(1 + 5 * l + k, r - L.pre[k]);
+  // select chain, not L.pre[k]: a dynamically indexed array would live in local memory,
+  // and every acquire poll invalidates L1 (CCTL.IVALL) -> an L2 round trip per lookup
+  const int k = r >= L.pre[4] ? 4 : r >= L.pre[3] ? 3 : r >= L.pre[2] ? 2 : r >= L.pre[1] ? 1 : 0;
+  const int base = k == 4 ? L.pre[4] : k == 3 ? L.pre[3] : k == 2 ? L.pre[2] : k == 1 ? L.pre[1] : 0;
+  return make_int2(1 + 5 * l + k, r - base);
 }
 AMUSD_DEV int phase_first(const FwArgs& a, const Lay& L, int p) {
   if (p == 0) return 0;
   const int l = layer_of(p), k = p == 1 + 5 * a.L ? 0 : (p - 1) % 5;
-  return KMAX + l * L.PL + (p == 1 + 5 * a.L ? 0 : L.pre[k]);
+  const int off = k == 4 ? L.pre[4] : k == 3 ? L.pre[3] : k == 2 ? L.pre[2] : k == 1 ? L.pre[1] : 0;
+  return KMAX + l * L.PL + off;
 }
 AMUSD_DEV int phase_count(const FwArgs& a, const Lay& L, int p) {
   const int kind = kind_of(p, a.L);
@@ -241,7 +247,7 @@ struct EpiSmem {
 // 16 token rows.  Activations written here are read by other CTAs of the same
 // launch: all loads/stores bypass L1 (.cg).
 AMUSD_DEV void tile_epilogue(const FwArgs& a, const GemmKind& ph, const __nv_bfloat16* gnext, int t, int nl,
-                             const float* v, int rows, EpiSmem* es, int q, int lane, const float* hpre = nullptr) {
+                             const float (&v)[BN], int rows, EpiSmem* es, int q, int lane) {
   const float* inv = es->inv;
   if (ph.epi == kEpStoreScaled) {
     const int n = t * BM + nl;
@@ -255,7 +261,7 @@ AMUSD_DEV void tile_epilogue(const FwArgs& a, const GemmKind& ph, const __nv_bfl
     for (int r = 0; r < BN; ++r) {
       float hn = 0.f;
       if (r < rows) {
-        hn = (hpre ? hpre[r] : __ldcg(ph.out + (size_t)r * ph.ldo + n)) + v[r];
+        hn = __ldcg(ph.out + (size_t)r * ph.ldo + n) + v[r];
         __stcg(ph.out + (size_t)r * ph.ldo + n, hn);
         ph.xnext[(size_t)r * ph.ldo + n] = __float2bfloat16(hn * gn);
       }
@@ -350,15 +356,63 @@ template <int HD, int G>
 struct AttnSmem {
   __nv_bfloat16 kb[kAttnChunk][HD];   // cached K rows of the chunk (bulk copy)
   __nv_bfloat16 vb[kAttnChunk][HD];   // cached V rows of the chunk (bulk copy)
-  float qs[G][HD];                    // rotated queries of the group
+  float qs[G * HD];                   // rotated queries, float4 chunks [G][lo/hi][HD/8] (attn_qidx)
   float kn[KMAX][HD];                 // this step's rotated K rows (bf16-rounded) ...
   float vn[KMAX][HD];                 // ... and V rows; red[4][G][HD] aliases kn/vn afterwards
-  float sc[G][kAttnChunk];            // scores -> probabilities
+  float sc[kAttnChunk][G];            // scores -> probabilities (position-major: one vector load per position)
   float stat[2][G];
   float wred[4][G];
   int last;
   uint64_t bar;                       // K/V bulk-copy completion
 };
+
+// Rotated-query layout: dims [8c, 8c+4) of head j at float4 (2j)*NC + c, [8c+4, 8c+8) at (2j+1)*NC + c.
+template <int HD>
+AMUSD_DEV int attn_qidx(int j, int e) {
+  constexpr int NC = HD / 8;
+  return ((2 * j + ((e >> 2) & 1)) * NC + (e >> 3)) * 4 + (e & 3);
+}
+template <int G, int NC>
+AMUSD_DEV void attn_dot8(float (&dot)[G], const float (&f)[8], const float4* qv, int c) {
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    const float4 qa = qv[2 * j * NC + c], qb = qv[(2 * j + 1) * NC + c];
+    dot[j] = fmaf(f[0], qa.x, dot[j]); dot[j] = fmaf(f[1], qa.y, dot[j]);
+    dot[j] = fmaf(f[2], qa.z, dot[j]); dot[j] = fmaf(f[3], qa.w, dot[j]);
+    dot[j] = fmaf(f[4], qb.x, dot[j]); dot[j] = fmaf(f[5], qb.y, dot[j]);
+    dot[j] = fmaf(f[6], qb.z, dot[j]); dot[j] = fmaf(f[7], qb.w, dot[j]);
+  }
+}
+// DPL consecutive bf16 of a cached V row (one 4- or 8-byte load)
+template <int DPL>
+AMUSD_DEV void attn_vrow(const __nv_bfloat16* v, float (&f)[DPL]) {
+  static_assert(DPL == 2 || DPL == 4, "DPL");
+  if constexpr (DPL == 4) {
+    const uint2 u = *(const uint2*)v;
+    const float2 a = __bfloat1622float2(*(const __nv_bfloat162*)&u.x), b = __bfloat1622float2(*(const __nv_bfloat162*)&u.y);
+    f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+  } else {
+    const float2 a = __bfloat1622float2(*(const __nv_bfloat162*)v);
+    f[0] = a.x; f[1] = a.y;
+  }
+}
+// the G probabilities of one position (vector loads)
+template <int G>
+AMUSD_DEV void attn_prow(const float* s, float (&p)[G]) {
+  if constexpr (G % 4 == 0) {
+#pragma unroll
+    for (int j = 0; j < G; j += 4) {
+      const float4 x = *(const float4*)(s + j);
+      p[j] = x.x; p[j + 1] = x.y; p[j + 2] = x.z; p[j + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < G; j += 2) {
+      const float2 x = *(const float2*)(s + j);
+      p[j] = x.x; p[j + 1] = x.y;
+    }
+  }
+}
 
 // Issue the bulk copies of the cached K/V rows [lo, min(hi, pos0)) of head g
 // (they do not depend on this step): called before the QKV dependency wait.
@@ -387,7 +441,7 @@ AMUSD_DEV bool attn_prefetch(const FwArgs& a, AttnSmem<HD, G>* sm, int layer, in
 // completes only the query rows cost a round trip.
 template <int HD, int G>
 AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint32_t bar_par, int layer, int g, int r,
-                         int split, int pos0, int tid) {
+                         int split, int pos0, int tid, int dbg_item = -1) {
   constexpr int DPL = HD / 32, NC = HD / 8;
   const int wi = tid >> 5, lane = tid & 31;
   float(*red)[G][HD] = (float(*)[G][HD])&sm->kn[0][0];
@@ -398,30 +452,56 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
   const int half = HD / 2, ncols = (a.H + 2 * a.KV) * HD;
   const float* qkv = a.qkv;
   const int qoff = g * (G + 2) * HD, koff = qoff + G * HD, voff = koff + HD;  // group-blocked q|k|v
-  for (int i = tid; i < G * half; i += 128) {
-    const int j = i / half, e = i - j * half;
-    const float* q = qkv + (size_t)r * ncols + qoff + j * HD;
-    const float c = a.cos[(size_t)p * half + e], s = a.sin[(size_t)p * half + e];
-    const float q0 = __ldcg(q + e), q1 = __ldcg(q + e + half);
-    sm->qs[j][e] = q0 * c - q1 * s;
-    sm->qs[j][e + half] = q1 * c + q0 * s;
-  }
+  // ---- gather: q rows of the group, this step's K/V window rows; RoPE; one L2 round
+  // trip (every load of a batch issued before any use)
   const int jmax = hi > pos0 ? min(r, hi - 1 - pos0) : -1;
-  for (int i = tid; i < (jmax + 1) * half; i += 128) {
-    const int j = i / half, e = i - j * half;
-    const int pj = pos0 + j;
-    const float* kr = qkv + (size_t)j * ncols + koff;
-    const float c = a.cos[(size_t)pj * half + e], s = a.sin[(size_t)pj * half + e];
-    const float k0 = __ldcg(kr + e), k1 = __ldcg(kr + e + half);
-    sm->kn[j][e] = __bfloat162float(__float2bfloat16(k0 * c - k1 * s));
-    sm->kn[j][e + half] = __bfloat162float(__float2bfloat16(k1 * c + k0 * s));
-  }
-  for (int i = tid; i < (jmax + 1) * HD; i += 128) {
-    const int j = i / HD, e = i - j * HD;
-    sm->vn[j][e] = __bfloat162float(__float2bfloat16(__ldcg(qkv + (size_t)j * ncols + voff + e)));
+  const int nq = G * half, nk = (jmax + 1) * half, ntot = nq + nk + (jmax + 1) * HD;
+  for (int b = tid; b < ntot; b += 128 * 4) {
+    float x0[4], x1[4], cs[4], sn[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = b + 128 * u;
+      x1[u] = cs[u] = sn[u] = 0.f;
+      if (i < nq) {
+        const int j = i / half, e = i - j * half;
+        const float* q = qkv + (size_t)r * ncols + qoff + j * HD + e;
+        x0[u] = __ldcg(q);
+        x1[u] = __ldcg(q + half);
+        cs[u] = a.cos[(size_t)p * half + e];
+        sn[u] = a.sin[(size_t)p * half + e];
+      } else if (i < nq + nk) {
+        const int i2 = i - nq, j = i2 / half, e = i2 - j * half;
+        const float* k = qkv + (size_t)j * ncols + koff + e;
+        x0[u] = __ldcg(k);
+        x1[u] = __ldcg(k + half);
+        cs[u] = a.cos[(size_t)(pos0 + j) * half + e];
+        sn[u] = a.sin[(size_t)(pos0 + j) * half + e];
+      } else if (i < ntot) {
+        const int i2 = i - nq - nk, j = i2 / HD, e = i2 - j * HD;
+        x0[u] = __ldcg(qkv + (size_t)j * ncols + voff + e);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = b + 128 * u;
+      const float r0 = x0[u] * cs[u] - x1[u] * sn[u], r1 = x1[u] * cs[u] + x0[u] * sn[u];
+      if (i < nq) {
+        const int j = i / half, e = i - j * half;
+        sm->qs[attn_qidx<HD>(j, e)] = r0;
+        sm->qs[attn_qidx<HD>(j, e + half)] = r1;
+      } else if (i < nq + nk) {
+        const int i2 = i - nq, j = i2 / half, e = i2 - j * half;
+        sm->kn[j][e] = __bfloat162float(__float2bfloat16(r0));
+        sm->kn[j][e + half] = __bfloat162float(__float2bfloat16(r1));
+      } else if (i < ntot) {
+        const int i2 = i - nq - nk, j = i2 / HD, e = i2 - j * HD;
+        sm->vn[j][e] = __bfloat162float(__float2bfloat16(x0[u]));
+      }
+    }
   }
   if (staged) mbar_wait_t(smem_u32(&sm->bar), bar_par);
   named_bar(1, 128);
+  if (a.dbg && tid == 0 && dbg_item >= 0) dbg_mark(a, dbg_item, 6, globaltimer());  // inputs ready
   if (p >= lo && p < hi) {  // KV append for row r (pending-token scheme)
     __nv_bfloat16* kc = (__nv_bfloat16*)(a.kcache + layer * a.kv_layer_bytes) + ((size_t)g * a.S + p) * HD;
     __nv_bfloat16* vc = (__nv_bfloat16*)(a.vcache + layer * a.kv_layer_bytes) + ((size_t)g * a.S + p) * HD;
@@ -430,7 +510,10 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
       vc[e] = __float2bfloat16(sm->vn[r][e]);
     }
   }
-  // ---- scores: thread per position (kAttnChunk == 128 == threads)
+  // ---- scores: thread per position (kAttnChunk == 128 == threads).  Chunk order rotated
+  // by tid & 7: the 8 threads of a quarter-warp read 8 distinct 16-byte bank groups of
+  // their K rows, and the warp reads 8 distinct (consecutive) query chunks.
+  const float4* qv = (const float4*)sm->qs;
   float mloc[G];
 #pragma unroll
   for (int j = 0; j < G; ++j) mloc[j] = -INFINITY;
@@ -444,17 +527,10 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
         const uint4* kt = (const uint4*)&sm->kb[t - lo][0];
 #pragma unroll 4
         for (int cc = 0; cc < NC; ++cc) {
-          const int c = (cc + tid) % NC;  // rotated: a quarter-warp touches 8 distinct 16-byte bank groups
+          const int c = (cc + (tid & 7)) & (NC - 1);
           float f[8];
           Elem<__nv_bfloat16>::unpack(kt[c], f);
-#pragma unroll
-          for (int j = 0; j < G; ++j) {
-            const float4 qa = *(const float4*)&sm->qs[j][8 * c], qb = *(const float4*)&sm->qs[j][8 * c + 4];
-            dot[j] = fmaf(f[0], qa.x, dot[j]); dot[j] = fmaf(f[1], qa.y, dot[j]);
-            dot[j] = fmaf(f[2], qa.z, dot[j]); dot[j] = fmaf(f[3], qa.w, dot[j]);
-            dot[j] = fmaf(f[4], qb.x, dot[j]); dot[j] = fmaf(f[5], qb.y, dot[j]);
-            dot[j] = fmaf(f[6], qb.z, dot[j]); dot[j] = fmaf(f[7], qb.w, dot[j]);
-          }
+          attn_dot8<G, NC>(dot, f, qv, c);
         }
       } else {
         // this step's keys: SAME summation order as the cached path (a position's score
@@ -462,27 +538,21 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
         const float* kr = sm->kn[t - pos0];
 #pragma unroll 4
         for (int cc = 0; cc < NC; ++cc) {
-          const int c = (cc + tid) % NC;
+          const int c = (cc + (tid & 7)) & (NC - 1);
           const float4 ka = *(const float4*)&kr[8 * c], kb4 = *(const float4*)&kr[8 * c + 4];
           const float f[8] = {ka.x, ka.y, ka.z, ka.w, kb4.x, kb4.y, kb4.z, kb4.w};
-#pragma unroll
-          for (int j = 0; j < G; ++j) {
-            const float4 qa = *(const float4*)&sm->qs[j][8 * c], qb = *(const float4*)&sm->qs[j][8 * c + 4];
-            dot[j] = fmaf(f[0], qa.x, dot[j]); dot[j] = fmaf(f[1], qa.y, dot[j]);
-            dot[j] = fmaf(f[2], qa.z, dot[j]); dot[j] = fmaf(f[3], qa.w, dot[j]);
-            dot[j] = fmaf(f[4], qb.x, dot[j]); dot[j] = fmaf(f[5], qb.y, dot[j]);
-            dot[j] = fmaf(f[6], qb.z, dot[j]); dot[j] = fmaf(f[7], qb.w, dot[j]);
-          }
+          attn_dot8<G, NC>(dot, f, qv, c);
         }
       }
 #pragma unroll
       for (int j = 0; j < G; ++j) {
         const float sv = dot[j] * a.scale;
-        sm->sc[j][t - lo] = sv;
+        sm->sc[t - lo][j] = sv;
         mloc[j] = sv;
       }
     }
   }
+  if (a.dbg && tid == 0 && dbg_item >= 0) dbg_mark(a, dbg_item, 2, globaltimer());  // scores done
   // ---- softmax statistics per head (fixed reduction tree)
 #pragma unroll
   for (int j = 0; j < G; ++j) {
@@ -499,8 +569,8 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
   if (lo + tid < hi) {
 #pragma unroll
     for (int j = 0; j < G; ++j) {
-      const float e = expf(sm->sc[j][tid] - mj[j]);
-      sm->sc[j][tid] = e;
+      const float e = expf(sm->sc[tid][j] - mj[j]);
+      sm->sc[tid][j] = e;
       lloc[j] = e;
     }
   }
@@ -511,34 +581,57 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
     if (lane == 0) sm->wred[wi][j] = l;
   }
   named_bar(1, 128);
-  if (tid < G) {
-    sm->stat[0][tid] = mj[tid];
-    sm->stat[1][tid] = (sm->wred[0][tid] + sm->wred[1][tid]) + (sm->wred[2][tid] + sm->wred[3][tid]);
+  if (wi == 0) {  // one warp records the per-head stats (mj[] stays in registers: constant indices)
+#pragma unroll
+    for (int j = 0; j < G; ++j)
+      if (lane == j) {
+        sm->stat[0][j] = mj[j];
+        sm->stat[1][j] = (sm->wred[0][j] + sm->wred[1][j]) + (sm->wred[2][j] + sm->wred[3][j]);
+      }
   }
   // ---- unnormalised P.V from shared memory: warp w takes positions lo+w, lo+w+4, ...
+  // (cached rows, then window rows: increasing t, the same order at every batch size)
   float acc[G][DPL];
 #pragma unroll
   for (int j = 0; j < G; ++j)
 #pragma unroll
     for (int e = 0; e < DPL; ++e) acc[j][e] = 0.f;
-  for (int t = lo + wi; t < hi; t += 4) {
-    float vv[DPL];
-    if (t < pos0) {
-      const __nv_bfloat16* vt = &sm->vb[t - lo][lane * DPL];
+  const int tce = min(hi, pos0);
+  int t = lo + wi;
+  for (; t + 12 < tce; t += 16) {  // 4 positions' loads in flight
+    float vv[4][DPL], pp[4][G];
 #pragma unroll
-      for (int e = 0; e < DPL; ++e) vv[e] = __bfloat162float(vt[e]);
-    } else {
-#pragma unroll
-      for (int e = 0; e < DPL; ++e) vv[e] = sm->vn[t - pos0][lane * DPL + e];
+    for (int u = 0; u < 4; ++u) {
+      attn_vrow<DPL>(&sm->vb[t + 4 * u - lo][lane * DPL], vv[u]);
+      attn_prow<G>(sm->sc[t + 4 * u - lo], pp[u]);
     }
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-      const float pj = sm->sc[j][t - lo];
+    for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int e = 0; e < DPL; ++e) acc[j][e] = fmaf(pj, vv[e], acc[j][e]);
-    }
+      for (int j = 0; j < G; ++j)
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) acc[j][e] = fmaf(pp[u][j], vv[u][e], acc[j][e]);
+  }
+  for (; t < tce; t += 4) {
+    float vv[DPL], pp[G];
+    attn_vrow<DPL>(&sm->vb[t - lo][lane * DPL], vv);
+    attn_prow<G>(sm->sc[t - lo], pp);
+#pragma unroll
+    for (int j = 0; j < G; ++j)
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) acc[j][e] = fmaf(pp[j], vv[e], acc[j][e]);
+  }
+  for (; t < hi; t += 4) {
+    float pp[G];
+    attn_prow<G>(sm->sc[t - lo], pp);
+    const float* vr = &sm->vn[t - pos0][lane * DPL];
+#pragma unroll
+    for (int j = 0; j < G; ++j)
+#pragma unroll
+      for (int e = 0; e < DPL; ++e) acc[j][e] = fmaf(pp[j], vr[e], acc[j][e]);
   }
   named_bar(1, 128);  // everyone is done with kn/vn before red overwrites them
+  if (a.dbg && tid == 0 && dbg_item >= 0) dbg_mark(a, dbg_item, 7, globaltimer());  // P.V done
 #pragma unroll
   for (int j = 0; j < G; ++j)
 #pragma unroll
@@ -554,19 +647,19 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
     }
     return;
   }
-  float* ws = a.attn_ws + (((size_t)g * KMAX + r) * a.max_splits + split) * G * (HD + 2);
-  for (int i = tid; i < G * HD; i += 128) {
-    const int j = i / HD, e = i - j * HD;
-    __stcg(ws + j * (HD + 2) + e, red[0][j][e] + red[1][j][e] + red[2][j][e] + red[3][j][e]);
-  }
-  if (tid < G) {
-    __stcg(ws + tid * (HD + 2) + HD, sm->stat[0][tid]);
-    __stcg(ws + tid * (HD + 2) + HD + 1, sm->stat[1][tid]);
-  }
-  named_bar(1, 128);
   // The row's last split (grabbed after its other splits) merges; the others publish and go.
   int* cnt = a.attn_cnt + (g * KMAX + r) * kPad;
   if (split != nsplit - 1) {
+    float* ws = a.attn_ws + (((size_t)g * KMAX + r) * a.max_splits + split) * G * (HD + 2);
+    for (int i = tid; i < G * HD; i += 128) {
+      const int j = i / HD, e = i - j * HD;
+      __stcg(ws + j * (HD + 2) + e, red[0][j][e] + red[1][j][e] + red[2][j][e] + red[3][j][e]);
+    }
+    if (tid < G) {
+      __stcg(ws + tid * (HD + 2) + HD, sm->stat[0][tid]);
+      __stcg(ws + tid * (HD + 2) + HD + 1, sm->stat[1][tid]);
+    }
+    named_bar(1, 128);
     if (tid == 0) red_add_release(cnt, 1);
     return;
   }
@@ -575,38 +668,58 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
     *cnt = 0;
   }
   named_bar(1, 128);
+  // Merge in split order, NB splits per batch with every load of the batch (all II output
+  // elements of this thread) in flight; this split's own partial comes from shared memory.
+  constexpr int II = G * HD / 128, NB = II <= 4 ? 4 : 2;
   const float* base = a.attn_ws + ((size_t)g * KMAX + r) * a.max_splits * G * (HD + 2);
-  for (int i = tid; i < G * HD; i += 128) {
-    const int j = i / HD, e = i - j * HD;
-    // splits in batches of 8 with every load of a batch in flight, merged in split order
-    float M = -INFINITY, Ls = 0.f, O = 0.f;
-    for (int b0 = 0; b0 < nsplit; b0 += 8) {
-      float m[8], l[8], o[8];
+  float M[II], Ls[II], O[II];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const float* w = base + ((size_t)(b0 + u) * G + j) * (HD + 2);
-        const bool ok = b0 + u < nsplit;
-        m[u] = ok ? __ldcg(w + HD) : -INFINITY;
-        l[u] = ok ? __ldcg(w + HD + 1) : 0.f;
-        o[u] = ok ? __ldcg(w + e) : 0.f;
-      }
-      float Mb = M;
+  for (int ii = 0; ii < II; ++ii) M[ii] = -INFINITY, Ls[ii] = 0.f, O[ii] = 0.f;
+  for (int b0 = 0; b0 < nsplit; b0 += NB) {
+    float m[II][NB], l[II][NB], o[II][NB];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) Mb = fmaxf(Mb, m[u]);
-      const float f0 = M == -INFINITY ? 0.f : expf(M - Mb);  // rescale the running sums
-      Ls *= f0;
-      O *= f0;
+    for (int ii = 0; ii < II; ++ii) {
+      const int i = tid + 128 * ii, j = i / HD, e = i - j * HD;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (b0 + u < nsplit) {
-          const float f = expf(m[u] - Mb);
-          Ls += l[u] * f;
-          O += o[u] * f;
+      for (int u = 0; u < NB; ++u) {
+        const int sp = b0 + u;
+        if (sp < nsplit - 1) {
+          const float* w = base + ((size_t)sp * G + j) * (HD + 2);
+          m[ii][u] = __ldcg(w + HD);
+          l[ii][u] = __ldcg(w + HD + 1);
+          o[ii][u] = __ldcg(w + e);
+        } else if (sp == nsplit - 1) {
+          m[ii][u] = sm->stat[0][j];
+          l[ii][u] = sm->stat[1][j];
+          o[ii][u] = red[0][j][e] + red[1][j][e] + red[2][j][e] + red[3][j][e];
+        } else {
+          m[ii][u] = -INFINITY, l[ii][u] = 0.f, o[ii][u] = 0.f;
         }
       }
-      M = Mb;
     }
-    out[(size_t)r * ldo + (g * G + j) * HD + e] = __float2bfloat16(O / Ls);
+#pragma unroll
+    for (int ii = 0; ii < II; ++ii) {
+      float Mb = M[ii];
+#pragma unroll
+      for (int u = 0; u < NB; ++u) Mb = fmaxf(Mb, m[ii][u]);
+      const float f0 = M[ii] == -INFINITY ? 0.f : expf(M[ii] - Mb);  // rescale the running sums
+      Ls[ii] *= f0;
+      O[ii] *= f0;
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        if (b0 + u < nsplit) {
+          const float f = expf(m[ii][u] - Mb);
+          Ls[ii] += l[ii][u] * f;
+          O[ii] += o[ii][u] * f;
+        }
+      }
+      M[ii] = Mb;
+    }
+  }
+#pragma unroll
+  for (int ii = 0; ii < II; ++ii) {
+    const int i = tid + 128 * ii, j = i / HD, e = i - j * HD;
+    out[(size_t)r * ldo + (g * G + j) * HD + e] = __float2bfloat16(O[ii] / Ls[ii]);
   }
 }
 
@@ -666,15 +779,21 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
   __syncthreads();
   if (!s_lay[3]) return;  // inactive step: nothing grabbed, nothing to reset
-  Lay L;
-  L.A = s_lay[0]; L.rows = s_lay[1]; L.pos0 = s_lay[2];
-  L.pre[0] = 0;
-  L.pre[1] = a.g[kGQkv].nitems;
-  L.pre[2] = L.pre[1] + L.A;
-  L.pre[3] = L.pre[2] + a.g[kGO].nitems;
-  L.pre[4] = L.pre[3] + a.g[kGGu].nitems;
-  L.PL = L.pre[4] + a.g[kGDown].nitems;
-  L.total = KMAX + a.L * L.PL + a.g[kGLm].nitems;
+  // The launch layout lives in shared memory: as a long-lived register struct it spills to
+  // local memory, and every acquire poll on the SM invalidates L1 (CCTL.IVALL), turning each
+  // reload into an L2 round trip.
+  __shared__ Lay s_L;
+  if (threadIdx.x == 0) {
+    s_L.A = s_lay[0]; s_L.rows = s_lay[1]; s_L.pos0 = s_lay[2];
+    s_L.pre[0] = 0;
+    s_L.pre[1] = a.g[kGQkv].nitems;
+    s_L.pre[2] = s_L.pre[1] + s_L.A;
+    s_L.pre[3] = s_L.pre[2] + a.g[kGO].nitems;
+    s_L.pre[4] = s_L.pre[3] + a.g[kGGu].nitems;
+    s_L.PL = s_L.pre[4] + a.g[kGDown].nitems;
+    s_L.total = KMAX + a.L * s_L.PL + a.g[kGLm].nitems;
+  }
+  const Lay& L = s_L;
   if (warp == kWarpMma0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "n"(kTmemCols));
@@ -841,6 +960,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         mbar_arrive(smem_u32(&qempty[slot]));
         ++n;
         if (it.x < 0) break;
+        const bool nomma = a.debug & 1;
         const int kind = kind_of(it.x, a.L);
         if (!is_gemm(kind)) continue;
         const int kc = a.g[gemm_of(kind)].kc;
@@ -854,7 +974,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           mbar_wait_t(smem_u32(&wfull[s]), par);
           mbar_wait_t(smem_u32(&xfull[s]), par);
           tc_fence_after();
-          if (a.debug & 1) {  // perf isolation: consume the stage without an MMA
+          if (nomma) {  // perf isolation: consume the stage without an MMA
             mbar_arrive(smem_u32(&empty[s]));
             continue;
           }
@@ -862,7 +982,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
                u > 0 ? 1u : 0u);
           umma_commit(smem_u32(&empty[s]));
         }
-        if (a.debug & 1) mbar_arrive(smem_u32(&tfull[b]));
+        if (nomma) mbar_arrive(smem_u32(&tfull[b]));
         else umma_commit(smem_u32(&tfull[b]));
         ++seg;
       }
@@ -948,8 +1068,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         // chunks it waits for.
         const int cj = j / g.ntiles, t = j - cj * g.ntiles;
         bool final = true;
-        float acc[BN], hpre[BN];
-        bool have_hpre = false;
+        float acc[BN];
         if (nchunks > 1) {
           // Split-K in exact int64 fixed point (2^-32): the red.adds commute, so the merged
           // tile is bit-identical whatever the chunks' arrival order (deterministic, batch
@@ -970,13 +1089,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
               else red_add_release(a.tile_cnt + g.cnt_off + t * kPad, 1);
             }
           } else {
-            // residual rows do not depend on this phase: load them while waiting for the chunks
-            if (epi == kEpResid) {
-#pragma unroll
-              for (int r = 0; r < BN; ++r)
-                hpre[r] = r < L.rows ? __ldcg(g.out + (size_t)r * g.ldo + t * BM + nl) : 0.f;
-              have_hpre = true;
-            }
             if (tid == 0) {
               wait_count(a.tile_cnt + g.cnt_off + t * kPad, nchunks - 1);
               a.tile_cnt[g.cnt_off + t * kPad] = 0;  // re-arm for the next phase / launch
@@ -998,7 +1110,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         }
         if (final) {
           const __nv_bfloat16* gnext = g.gnext ? g.gnext + (size_t)layer * g.gnext_stride : nullptr;
-          tile_epilogue(a, g, gnext, t, nl, acc, L.rows, es, q, lane, have_hpre ? hpre : nullptr);
+          tile_epilogue(a, g, gnext, t, nl, acc, L.rows, es, q, lane);
         }
         wrote = final;
         lm_last_check = epi == kEpArgmax;
@@ -1033,13 +1145,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
         named_bar(1, 128);
         staged = asm_->last;
         if (a.dbg && tid == 0) dbg_mark(a, phase_first(a, L, p) + j, 3, globaltimer());
-        attn_item<HD, G>(a, asm_, staged, attn_par, layer, gh, r, split, L.pos0, tid);
+        attn_item<HD, G>(a, asm_, staged, attn_par, layer, gh, r, split, L.pos0, tid, phase_first(a, L, p) + j);
         if (a.dbg && tid == 0) dbg_mark(a, phase_first(a, L, p) + j, 4, globaltimer());
         if (staged) attn_par ^= 1u;
       }
       // publish: this item's writes are visible (generic and async proxy) before the count
       // (CTA barrier, then one release by thread 0: the cooperative-groups grid-sync pattern).
-      if (a.dbg && tid == 0) dbg_mark(a, phase_first(a, L, p) + j, 7, globaltimer());
+      // (attention items: slot 2 = scores done, 6 = inputs ready, 7 = P.V done -- set in attn_item)
+      if (a.dbg && tid == 0 && kind != kKAttn) dbg_mark(a, phase_first(a, L, p) + j, 7, globaltimer());
       if (wrote) fence_proxy_async();
       named_bar(1, 128);
       if (tid == 0) {

@@ -2,6 +2,8 @@
 
   python tools/fw_timeline.py [--model 8b] [--layers 8] [--rows 1] --out gpurun_out/tl.npy
 Columns: item, cta, phase, t_grab, t_issued, t_dep, t_mma, t_done, t_waited, t_epi_done (ns, globaltimer).
+Attention items: t_issued = scores done, t_waited = inputs gathered, t_epi_done = P.V done,
+t_dep = QKV dependency seen, t_mma = item returned.
 """
 import argparse
 import ctypes as C
