@@ -525,7 +525,7 @@ int amusd_tf_create(amusd_model** out, const amusd_tf_config* cfg, const amusd_t
       size_t wsf;
       int mt, cints;
       fw::build_kinds(v, fw_units(), &m->fw_args, &wsf, &cints, &mt);
-      m->fw_ready = e == cudaSuccess;
+      m->fw_ready = e == cudaSuccess && c.max_seq <= fw::max_positions();  // else the per-kernel path
       m->fw_grid = num_sms();
       m->fw_stages = env_int("AMUSD_FW_STAGES", fw_max_stages(c, 1));
     }

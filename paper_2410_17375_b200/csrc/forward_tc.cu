@@ -52,7 +52,8 @@ constexpr int kThreads = 320;
 constexpr int kWarpX = 1, kWarpMma0 = 2, kWarpEpi0 = 6;
 constexpr int kTbuf = 4;                 // TMEM accumulator buffers (MMA may run 3 items ahead of the epilogue)
 constexpr int kTmemCols = kTbuf * NACC * BN;  // 256
-constexpr int kAttnChunk = 128;        // positions per attention split (K/V chunk staged in smem)
+constexpr int kMaxMerge = 128;         // max position splits of one row (8192 positions)
+constexpr int kAttnChunk = 64;         // positions per attention split (K/V chunk staged in smem; 2 threads each)
 constexpr long long kWaitNs = 4ll * 1000 * 1000 * 1000;  // dependency waits trap after 4 s
 // Every schedule counter owns a 128-byte line (grab counter, exit counter, one
 // per phase, one per split-K tile): 148 CTAs poll and bump them concurrently.
@@ -354,11 +355,11 @@ AMUSD_DEV void embed_item(const FwArgs& a, int r, int rows, int tid) {
 // Attention scratch layout (epilogue warps only).
 template <int HD, int G>
 struct AttnSmem {
-  __nv_bfloat16 kb[kAttnChunk][HD];   // cached K rows of the chunk (bulk copy)
+  __nv_bfloat16 kb[kAttnChunk][HD];   // cached K rows of the chunk (bulk copy); red[4][G][HD] aliases it after P.V
   __nv_bfloat16 vb[kAttnChunk][HD];   // cached V rows of the chunk (bulk copy)
   float qs[G * HD];                   // rotated queries, float4 chunks [G][lo/hi][HD/8] (attn_qidx)
-  float kn[KMAX][HD];                 // this step's rotated K rows (bf16-rounded) ...
-  float vn[KMAX][HD];                 // ... and V rows; red[4][G][HD] aliases kn/vn afterwards
+  __nv_bfloat16 kn[KMAX][HD];         // this step's rotated K rows (bf16, exactly as the cache holds them)
+  __nv_bfloat16 vn[KMAX][HD];         // ... and V rows
   float sc[kAttnChunk][G];            // scores -> probabilities (position-major: one vector load per position)
   float stat[2][G];
   float wred[4][G];
@@ -444,8 +445,8 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
                          int split, int pos0, int tid, int dbg_item = -1) {
   constexpr int DPL = HD / 32, NC = HD / 8;
   const int wi = tid >> 5, lane = tid & 31;
-  float(*red)[G][HD] = (float(*)[G][HD])&sm->kn[0][0];
-  static_assert(4 * G <= 2 * KMAX, "red alias");
+  float(*red)[G][HD] = (float(*)[G][HD])&sm->kb[0][0];
+  static_assert(4 * G * HD * 4 <= kAttnChunk * HD * 2, "red alias");
   const int p = pos0 + r;
   const int nsplit = nsplit_of(p);
   const int lo = split * kAttnChunk, hi = min(p + 1, lo + kAttnChunk);
@@ -491,11 +492,11 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
         sm->qs[attn_qidx<HD>(j, e + half)] = r1;
       } else if (i < nq + nk) {
         const int i2 = i - nq, j = i2 / half, e = i2 - j * half;
-        sm->kn[j][e] = __bfloat162float(__float2bfloat16(r0));
-        sm->kn[j][e + half] = __bfloat162float(__float2bfloat16(r1));
+        sm->kn[j][e] = __float2bfloat16(r0);
+        sm->kn[j][e + half] = __float2bfloat16(r1);
       } else if (i < ntot) {
         const int i2 = i - nq - nk, j = i2 / HD, e = i2 - j * HD;
-        sm->vn[j][e] = __bfloat162float(__float2bfloat16(x0[u]));
+        sm->vn[j][e] = __float2bfloat16(x0[u]);
       }
     }
   }
@@ -506,48 +507,43 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
     __nv_bfloat16* kc = (__nv_bfloat16*)(a.kcache + layer * a.kv_layer_bytes) + ((size_t)g * a.S + p) * HD;
     __nv_bfloat16* vc = (__nv_bfloat16*)(a.vcache + layer * a.kv_layer_bytes) + ((size_t)g * a.S + p) * HD;
     for (int e = tid; e < HD; e += 128) {
-      kc[e] = __float2bfloat16(sm->kn[r][e]);
-      vc[e] = __float2bfloat16(sm->vn[r][e]);
+      kc[e] = sm->kn[r][e];
+      vc[e] = sm->vn[r][e];
     }
   }
-  // ---- scores: thread per position (kAttnChunk == 128 == threads).  Chunk order rotated
-  // by tid & 7: the 8 threads of a quarter-warp read 8 distinct 16-byte bank groups of
-  // their K rows, and the warp reads 8 distinct (consecutive) query chunks.
+  // ---- scores: a thread pair per position (kAttnChunk == 64, 128 threads), each thread one
+  // half of the head dims, then one shuffle.  Chunk order rotated so the 8 threads of a
+  // quarter-warp read 8 distinct 16-byte bank groups of their K rows and the warp reads few
+  // distinct query chunks.  Cached and window keys use the SAME order (batch invariance: a
+  // position's score must not depend on whether it is in the cache or the window).
   const float4* qv = (const float4*)sm->qs;
+  constexpr int NH = NC / 2;  // 16-byte chunks per half row
+  const int pi = tid >> 1, hf = tid & 1;
   float mloc[G];
 #pragma unroll
   for (int j = 0; j < G; ++j) mloc[j] = -INFINITY;
   {
-    const int t = lo + tid;
-    if (t < hi) {
-      float dot[G];
+    const int t = lo + pi;
+    float dot[G];
 #pragma unroll
-      for (int j = 0; j < G; ++j) dot[j] = 0.f;
-      if (t < pos0) {
-        const uint4* kt = (const uint4*)&sm->kb[t - lo][0];
+    for (int j = 0; j < G; ++j) dot[j] = 0.f;
+    if (t < hi) {
+      const uint4* kt = (const uint4*)(t < pos0 ? &sm->kb[t - lo][0] : &sm->kn[t - pos0][0]);
 #pragma unroll 4
-        for (int cc = 0; cc < NC; ++cc) {
-          const int c = (cc + (tid & 7)) & (NC - 1);
-          float f[8];
-          Elem<__nv_bfloat16>::unpack(kt[c], f);
-          attn_dot8<G, NC>(dot, f, qv, c);
-        }
-      } else {
-        // this step's keys: SAME summation order as the cached path (a position's score
-        // must not depend on whether it is in the cache or the window: batch invariance)
-        const float* kr = sm->kn[t - pos0];
-#pragma unroll 4
-        for (int cc = 0; cc < NC; ++cc) {
-          const int c = (cc + (tid & 7)) & (NC - 1);
-          const float4 ka = *(const float4*)&kr[8 * c], kb4 = *(const float4*)&kr[8 * c + 4];
-          const float f[8] = {ka.x, ka.y, ka.z, ka.w, kb4.x, kb4.y, kb4.z, kb4.w};
-          attn_dot8<G, NC>(dot, f, qv, c);
-        }
+      for (int cc = 0; cc < NH; ++cc) {
+        const int c = hf * NH + ((HD == 128 ? cc + (tid & 7) : cc + pi) & (NH - 1));
+        float f[8];
+        Elem<__nv_bfloat16>::unpack(kt[c], f);
+        attn_dot8<G, NC>(dot, f, qv, c);
       }
+    }
+#pragma unroll
+    for (int j = 0; j < G; ++j) dot[j] += __shfl_xor_sync(0xffffffffu, dot[j], 1);
+    if (t < hi) {
 #pragma unroll
       for (int j = 0; j < G; ++j) {
         const float sv = dot[j] * a.scale;
-        sm->sc[t - lo][j] = sv;
+        if (hf == 0) sm->sc[t - lo][j] = sv;
         mloc[j] = sv;
       }
     }
@@ -566,7 +562,7 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
     mj[j] = fmaxf(fmaxf(sm->wred[0][j], sm->wred[1][j]), fmaxf(sm->wred[2][j], sm->wred[3][j]));
     lloc[j] = 0.f;
   }
-  if (lo + tid < hi) {
+  if (tid < kAttnChunk && lo + tid < hi) {
 #pragma unroll
     for (int j = 0; j < G; ++j) {
       const float e = expf(sm->sc[tid][j] - mj[j]);
@@ -622,15 +618,15 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
       for (int e = 0; e < DPL; ++e) acc[j][e] = fmaf(pp[j], vv[e], acc[j][e]);
   }
   for (; t < hi; t += 4) {
-    float pp[G];
+    float vv[DPL], pp[G];
+    attn_vrow<DPL>(&sm->vn[t - pos0][lane * DPL], vv);
     attn_prow<G>(sm->sc[t - lo], pp);
-    const float* vr = &sm->vn[t - pos0][lane * DPL];
 #pragma unroll
     for (int j = 0; j < G; ++j)
 #pragma unroll
-      for (int e = 0; e < DPL; ++e) acc[j][e] = fmaf(pp[j], vr[e], acc[j][e]);
+      for (int e = 0; e < DPL; ++e) acc[j][e] = fmaf(pp[j], vv[e], acc[j][e]);
   }
-  named_bar(1, 128);  // everyone is done with kn/vn before red overwrites them
+  named_bar(1, 128);  // everyone is done with kb before red overwrites it
   if (a.dbg && tid == 0 && dbg_item >= 0) dbg_mark(a, dbg_item, 7, globaltimer());  // P.V done
 #pragma unroll
   for (int j = 0; j < G; ++j)
@@ -668,58 +664,69 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
     *cnt = 0;
   }
   named_bar(1, 128);
-  // Merge in split order, NB splits per batch with every load of the batch (all II output
-  // elements of this thread) in flight; this split's own partial comes from shared memory.
-  constexpr int II = G * HD / 128, NB = II <= 4 ? 4 : 2;
+  // Merge: (1) every split's (m, l) into shared memory (one round trip; this split's own
+  // from shared memory), (2) M = max m, weights w_s = exp(m_s - M), L = sum l_s w_s in split
+  // order, (3) O = sum o_s w_s in split order, 8 splits' loads in flight per batch.
+  // Deterministic and position-only (batch invariant).
   const float* base = a.attn_ws + ((size_t)g * KMAX + r) * a.max_splits * G * (HD + 2);
-  float M[II], Ls[II], O[II];
+  // [kMaxMerge][G] m (then the weights) and l, in the V staging buffer (dead after P.V)
+  float* wts = (float*)&sm->vb[0][0];
+  float* mlv = wts + kMaxMerge * G;
+  static_assert(2 * kMaxMerge * G * 4 <= kAttnChunk * HD * 2, "merge scratch alias");
+  for (int i = tid; i < nsplit * G; i += 128) {
+    const int sp = i / G, j = i - sp * G;
+    float m, l;
+    if (sp < nsplit - 1) {
+      const float* w = base + ((size_t)sp * G + j) * (HD + 2);
+      m = __ldcg(w + HD);
+      l = __ldcg(w + HD + 1);
+    } else {
+      m = sm->stat[0][j];
+      l = sm->stat[1][j];
+    }
+    wts[i] = m;
+    mlv[i] = l;
+  }
+  named_bar(1, 128);
+  if (tid < G) {
+    float M = -INFINITY;
+    for (int sp = 0; sp < nsplit; ++sp) M = fmaxf(M, wts[sp * G + tid]);
+    float Ls = 0.f;
+    for (int sp = 0; sp < nsplit; ++sp) {
+      const float w = expf(wts[sp * G + tid] - M);
+      wts[sp * G + tid] = w;
+      Ls += mlv[sp * G + tid] * w;
+    }
+    sm->stat[1][tid] = Ls;  // (own stat no longer needed)
+  }
+  named_bar(1, 128);
+  constexpr int II = G * HD / 128;
+  float O[II];
 #pragma unroll
-  for (int ii = 0; ii < II; ++ii) M[ii] = -INFINITY, Ls[ii] = 0.f, O[ii] = 0.f;
-  for (int b0 = 0; b0 < nsplit; b0 += NB) {
-    float m[II][NB], l[II][NB], o[II][NB];
+  for (int ii = 0; ii < II; ++ii) O[ii] = 0.f;
+  for (int b0 = 0; b0 < nsplit - 1; b0 += 8) {  // remote splits
+    float o[II][8];
 #pragma unroll
     for (int ii = 0; ii < II; ++ii) {
       const int i = tid + 128 * ii, j = i / HD, e = i - j * HD;
 #pragma unroll
-      for (int u = 0; u < NB; ++u) {
-        const int sp = b0 + u;
-        if (sp < nsplit - 1) {
-          const float* w = base + ((size_t)sp * G + j) * (HD + 2);
-          m[ii][u] = __ldcg(w + HD);
-          l[ii][u] = __ldcg(w + HD + 1);
-          o[ii][u] = __ldcg(w + e);
-        } else if (sp == nsplit - 1) {
-          m[ii][u] = sm->stat[0][j];
-          l[ii][u] = sm->stat[1][j];
-          o[ii][u] = red[0][j][e] + red[1][j][e] + red[2][j][e] + red[3][j][e];
-        } else {
-          m[ii][u] = -INFINITY, l[ii][u] = 0.f, o[ii][u] = 0.f;
-        }
-      }
+      for (int u = 0; u < 8; ++u)
+        o[ii][u] = b0 + u < nsplit - 1 ? __ldcg(base + ((size_t)(b0 + u) * G + j) * (HD + 2) + e) : 0.f;
     }
 #pragma unroll
     for (int ii = 0; ii < II; ++ii) {
-      float Mb = M[ii];
+      const int j = (tid + 128 * ii) / HD;
 #pragma unroll
-      for (int u = 0; u < NB; ++u) Mb = fmaxf(Mb, m[ii][u]);
-      const float f0 = M[ii] == -INFINITY ? 0.f : expf(M[ii] - Mb);  // rescale the running sums
-      Ls[ii] *= f0;
-      O[ii] *= f0;
-#pragma unroll
-      for (int u = 0; u < NB; ++u) {
-        if (b0 + u < nsplit) {
-          const float f = expf(m[ii][u] - Mb);
-          Ls[ii] += l[ii][u] * f;
-          O[ii] += o[ii][u] * f;
-        }
-      }
-      M[ii] = Mb;
+      for (int u = 0; u < 8; ++u)
+        if (b0 + u < nsplit - 1) O[ii] = fmaf(o[ii][u], wts[(b0 + u) * G + j], O[ii]);
     }
   }
 #pragma unroll
-  for (int ii = 0; ii < II; ++ii) {
+  for (int ii = 0; ii < II; ++ii) {  // own split last, then normalise
     const int i = tid + 128 * ii, j = i / HD, e = i - j * HD;
-    out[(size_t)r * ldo + (g * G + j) * HD + e] = __float2bfloat16(O[ii] / Ls[ii]);
+    const float own = red[0][j][e] + red[1][j][e] + red[2][j][e] + red[3][j][e];
+    O[ii] = fmaf(own, wts[(nsplit - 1) * G + j], O[ii]);
+    out[(size_t)r * ldo + (g * G + j) * HD + e] = __float2bfloat16(O[ii] / sm->stat[1][j]);
   }
 }
 
@@ -783,7 +790,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
   // local memory, and every acquire poll on the SM invalidates L1 (CCTL.IVALL), turning each
   // reload into an L2 round trip.
   __shared__ Lay s_L;
+  __shared__ int s_epi_done;  // items the epilogue warps have finished (producer: lazy attention grabs)
   if (threadIdx.x == 0) {
+    s_epi_done = 0;
     s_L.A = s_lay[0]; s_L.rows = s_lay[1]; s_L.pos0 = s_lay[2];
     s_L.pre[0] = 0;
     s_L.pre[1] = a.g[kGQkv].nitems;
@@ -837,10 +846,22 @@ __global__ void __launch_bounds__(kThreads, MINB)
       if (ahead > 0)  // the first `ahead` items have no earlier grabber: spread them over the CTAs
         for (int k = blockIdx.x; k < ahead; k += gridDim.x) prefetch_item(k);
       int i_next = atomicAdd(a.sched, 1);  // grab counter: sched[0]; exit counter: sched[kPad]
+      // Attention items go to drained CTAs: grabbed eagerly behind a GEMM still in flight, an
+      // attention item (and its row's split merge) would wait for that GEMM's whole epilogue.
+      auto attn_at = [&](int k) { return k < L.total && kind_of(locate(a, L, k).x, a.L) == kKAttn; };
       for (;;) {
-        // the grab of the following item is in flight while this one streams
+        // the grab of the following item is in flight while this one streams (GEMM items)
+        // (only QKV and attention items can be followed by an attention grab: the others
+        // grab eagerly, without the peek's round trip)
         const int i = i_next;
-        if (i < L.total) i_next = atomicAdd(a.sched, 1);
+        bool have_next = false;
+        if (i < L.total) {
+          const int k = kind_of(locate(a, L, i).x, a.L);
+          if (k != kKQkv && k != kKAttn) {
+            i_next = atomicAdd(a.sched, 1);
+            have_next = true;
+          }
+        }
         if (ahead > 0 && i < L.total) prefetch_item(i + ahead);
         const int slot = n % kQ;
         mbar_wait_t(smem_u32(&qempty[slot]), ((n / kQ) & 1) ^ 1);
@@ -888,6 +909,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
               bulk_load(smem_u32(sW + s * kWBytes), src + (size_t)u * kWBytes, kWBytes, smem_u32(&wfull[s]), pol_w);
           }
           dbg_mark(a, i, 2, globaltimer());
+        }
+        if (!have_next) {  // peek; an attention item waits until this CTA's pipeline has drained
+          for (;;) {
+            if (!attn_at(ld_volatile(a.sched))) break;
+            if (ld_volatile(&s_epi_done) >= n) break;
+            __nanosleep(64);
+          }
+          i_next = atomicAdd(a.sched, 1);
         }
       }
     }
@@ -1187,6 +1216,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           // acquire of the phase count reaches the final items' releases through the RMW chain
           red_add_relaxed(done + p * kPad, 1);
         }
+        *(volatile int*)&s_epi_done = n;  // item n done (the producer's lazy attention grab)
       }
     }
   }
@@ -1212,6 +1242,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
 // ------------------------------------------------------------ host side
 int attn_items_max(int KV, int S) { return KV * KMAX * attn_splits(S); }
 int attn_splits(int S) { return (S + kAttnChunk - 1) / kAttnChunk; }
+int max_positions() { return kMaxMerge * kAttnChunk; }
 
 static int pick_kc(int kb, int target) {
   int best = 1;

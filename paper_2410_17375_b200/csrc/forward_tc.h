@@ -86,7 +86,8 @@ struct FwArgs {
 __host__ __device__ inline int num_phases(int L) { return 2 + 5 * L; }
 constexpr int kCounterInts = 32;  // ints per schedule counter (one 128-byte line)
 int attn_items_max(int KV, int S);
-int attn_splits(int S);  // position splits of the persistent forward's attention (128-position chunks)
+int attn_splits(int S);  // position splits of the persistent forward's attention (64-position chunks)
+int max_positions();     // longest context (max_seq) the persistent forward's split merge supports
 
 // Host: fill the GEMM kinds of a model (tiled weights laid out per layer as
 // [qkv | o | gate-up | down], LM head after the last layer).

@@ -34,8 +34,11 @@ def worker(rank, port, n):
         ar = P.decode_autoregressive(m, prompt, cfg).tokens if link.role == "verify" else None
         peer_ar = link.exchange(ar)
         toks = ar if link.role == "verify" else peer_ar
-        print(json.dumps({"role": link.role, "tokens": res.tokens, "ar": toks, "rollbacks": res.stats.rollbacks,
-                          "ms": ms}), flush=True)
+        # one write(2) per line (< PIPE_BUF): the two ranks share the pipe and must not interleave
+        line = json.dumps({"role": link.role, "tokens": res.tokens, "ar": toks, "rollbacks": res.stats.rollbacks,
+                           "ms": ms}) + "\n"
+        sys.stdout.flush()
+        os.write(sys.stdout.fileno(), line.encode())
     except Exception:
         traceback.print_exc()
         sys.exit(1)
