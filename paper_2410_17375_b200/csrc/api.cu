@@ -113,6 +113,11 @@ struct amusd_model {
   float* fw_ws = nullptr;
   int* fw_tile_cnt = nullptr;
   int fw_grid = 0, fw_stages = 0;  // launch shape (set per engine at graph capture)
+  fw::ModelView fw_view{};          // persistent-forward model view (kinds rebuilt per grid)
+  fw::GemmKind fw_kinds_part[fw::kNumGemm];  // kinds for a partial-grid launch ...
+  int fw_part_grid = 0;             // ... built for this many SMs (0 = none yet)
+  bool fw_part_ok = false;          // draft role only: split-K chunking changes the fp32 partials,
+                                    // so the verify keeps one chunking in every engine (AR parity)
   int grid_override = 0;            // amusd_model_set_grid: SMs of amusd_time_forward launches (0 = all)
   int path = AMUSD_PATH_PERSISTENT;
   long long* fw_dbg = nullptr;  // optional per-item timeline (amusd_model_set_timeline)
@@ -398,6 +403,17 @@ static bool use_tc(const amusd_model* m, int nr) {
 static int fw_forward(amusd_model* m, StepCtl* ctl, cudaStream_t st, bool want_logits) {
   const amusd_tf_config& c = m->cfg;
   fw::FwArgs a = m->fw_args;
+  if (m->fw_part_ok && m->fw_grid < num_sms()) {  // co-located AMUSD draft: larger work items
+    if (m->fw_part_grid != m->fw_grid) {
+      fw::FwArgs t = m->fw_args;
+      size_t wsf;
+      int ci, mt;
+      fw::build_kinds(m->fw_view, fw_units(), &t, &wsf, &ci, &mt, m->fw_grid);
+      std::memcpy(m->fw_kinds_part, t.g, sizeof(t.g));
+      m->fw_part_grid = m->fw_grid;
+    }
+    std::memcpy(a.g, m->fw_kinds_part, sizeof(a.g));
+  }
   a.ctl = ctl; a.sched = m->fw_sched;
   a.embed = (const __nv_bfloat16*)m->w.embed; a.norms = m->fw_norms;
   a.h = m->h; a.xa = m->xa_b; a.ssp = m->ssp; a.qkv = m->qkv; a.attn_b = m->attn_b;
@@ -525,6 +541,7 @@ int amusd_tf_create(amusd_model** out, const amusd_tf_config* cfg, const amusd_t
       size_t wsf;
       int mt, cints;
       fw::build_kinds(v, fw_units(), &m->fw_args, &wsf, &cints, &mt);
+      m->fw_view = v;
       m->fw_ready = e == cudaSuccess && c.max_seq <= fw::max_positions();  // else the per-kernel path
       m->fw_grid = num_sms();
       m->fw_stages = env_int("AMUSD_FW_STAGES", fw_max_stages(c, 1));
@@ -969,6 +986,7 @@ static int capture_body(amusd_session* s, int engine, int actor, cudaGraph_t bod
     m->fw_stages = env_int("AMUSD_FW_STAGES", fw_max_stages(m->cfg, 1));
     m->fw_grid = num_sms();
     if (colo) m->fw_grid = m == s->draft ? draft_sms : num_sms() - draft_sms;
+    m->fw_part_ok = colo && m == s->draft;
   }
   auto fwd = [&](amusd_model* m, StepCtl* c, int nr) { if (!r) r = model_forward(m, c, nr, st, pdl, false); };
   auto pk = [&](int which, int arg) { if (!r && proto_launch(which, a, st, arg) != cudaSuccess) r = fail(AMUSD_ERR_CUDA, "protocol launch failed"); };
@@ -989,6 +1007,7 @@ static int capture_body(amusd_session* s, int engine, int actor, cudaGraph_t bod
   cudaError_t e = cudaStreamEndCapture(st, &g2);
   for (amusd_model* m : {s->draft, s->verify}) {  // parity API launches own the GPU again
     if (!m || !use_fw(m)) continue;
+    m->fw_part_ok = false;
     m->fw_stages = env_int("AMUSD_FW_STAGES", fw_max_stages(m->cfg, 1));
     m->fw_grid = num_sms();
   }

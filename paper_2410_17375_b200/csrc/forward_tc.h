@@ -107,7 +107,10 @@ struct ModelView {
 };
 // ws_floats: int64 accumulator regions of all kinds (in float units); cnt_ints: tile counters;
 // max_tiles: largest producer tile count (flag region size).
-void build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_floats, int* cnt_ints, int* max_tiles);
+// grid > 0: kinds for a launch on `grid` (< all) SMs (larger items, see forward_tc.cu); the
+// accumulator / counter needs never exceed the grid = 0 build's.
+void build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_floats, int* cnt_ints, int* max_tiles,
+                 int grid = 0);
 
 cudaError_t launch_forward(const FwArgs& a, const CUtensorMap& m_xa, const CUtensorMap& m_attn,
                            const CUtensorMap& m_act, const CUtensorMap& m_xb, int grid, int stages, cudaStream_t st);

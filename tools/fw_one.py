@@ -1,6 +1,6 @@
 """One model, a few eager persistent forwards (ncu target).
 
-  python tools/fw_one.py [--model 8b|1b] [--layers N] [--rows R] [--iters K] [--path persistent]
+  python tools/fw_one.py [--model 8b|1b] [--layers N] [--rows R] [--iters K] [--path persistent] [--grid SMS]
 """
 import argparse
 import ctypes as C
@@ -19,6 +19,7 @@ ap.add_argument("--rows", type=int, default=1)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--pos", type=int, default=300)
 ap.add_argument("--path", default="persistent")
+ap.add_argument("--grid", type=int, default=0, help="SMs of the persistent launch (0 = all)")
 a = ap.parse_args()
 TC = P.TransformerConfig
 kw = {"max_seq": max(640, a.pos + 64)}
@@ -29,6 +30,7 @@ m = P.TransformerModel(cfg, seed=3)
 m.set_path(a.path)
 m.init_state([(1234 * (i + 7)) % 31990 + 3 for i in range(a.pos)])
 ms = C.c_float()
+L.check(L.load().amusd_model_set_grid(m.handle, a.grid))
 L.check(L.load().amusd_time_forward(m.handle, a.rows, -1, 0, a.iters, C.byref(ms), device_stream(m.device)))
 gb = cfg.step_weight_bytes() / 1e9
 print(f"{a.model} L={cfg.n_layers} rows={a.rows} {ms.value:.4f} ms  {gb / ms.value * 1e3:.1f} GB/s")
