@@ -913,7 +913,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         if (!have_next) {  // peek; an attention item waits until this CTA's pipeline has drained
           for (;;) {
             if (!attn_at(ld_volatile(a.sched))) break;
-            if (ld_volatile(&s_epi_done) >= n) break;
+            if (atomicAdd(&s_epi_done, 0) >= n) break;  // (shared atomics: a race-free flag)
             __nanosleep(64);
           }
           i_next = atomicAdd(a.sched, 1);
@@ -1216,7 +1216,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           // acquire of the phase count reaches the final items' releases through the RMW chain
           red_add_relaxed(done + p * kPad, 1);
         }
-        *(volatile int*)&s_epi_done = n;  // item n done (the producer's lazy attention grab)
+        atomicExch(&s_epi_done, n);  // item n done (the producer's lazy attention grab)
       }
     }
   }

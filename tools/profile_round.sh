@@ -11,4 +11,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_fo
   -o gpurun_out/full -f python tools/ncu_forward.py > gpurun_out/ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_forward -s 7 -c 1 \
   -o gpurun_out/full_draft -f python tools/ncu_forward.py > gpurun_out/ncu_full_draft.log 2>&1
-tail -2 gpurun_out/ncu_launch.log gpurun_out/ncu_full.log gpurun_out/ncu_full_draft.log
+tail -n 2 gpurun_out/ncu_launch.log gpurun_out/ncu_full.log gpurun_out/ncu_full_draft.log
