@@ -235,12 +235,16 @@ AMUSD_DEV GemmRes resolve(const FwArgs& a, int gk, int layer) {
 }
 
 // ------------------------------------------------------------ epilogues
-struct EpiSmem {
+// Per-item epilogue temporaries: alias the attention K staging buffer (both belong to the
+// epilogue warps, which run one item at a time; the attention mbarrier stays outside).
+struct EpiTmp {
   float xchg[64 * BN];                // gate/up exchange
   unsigned long long kx[4 * BN];      // argmax per lane-quarter
   float sq[4 * BN];                   // residual sum-of-squares per lane-quarter
+};
+// Epilogue state that persists across items (the RMSNorm scale of the current phase).
+struct EpiSmem {
   float inv[BN];
-  int flag;
   int inv_phase;
 };
 
@@ -248,7 +252,7 @@ struct EpiSmem {
 // 16 token rows.  Activations written here are read by other CTAs of the same
 // launch: all loads/stores bypass L1 (.cg).
 AMUSD_DEV void tile_epilogue(const FwArgs& a, const GemmKind& ph, const __nv_bfloat16* gnext, int t, int nl,
-                             const float (&v)[BN], int rows, EpiSmem* es, int q, int lane) {
+                             const float (&v)[BN], int rows, EpiSmem* es, EpiTmp* et, int q, int lane) {
   const float* inv = es->inv;
   if (ph.epi == kEpStoreScaled) {
     const int n = t * BM + nl;
@@ -267,18 +271,18 @@ AMUSD_DEV void tile_epilogue(const FwArgs& a, const GemmKind& ph, const __nv_bfl
         ph.xnext[(size_t)r * ph.ldo + n] = __float2bfloat16(hn * gn);
       }
       const float s2 = warp_sum(hn * hn);
-      if (lane == 0) es->sq[q * BN + r] = s2;
+      if (lane == 0) et->sq[q * BN + r] = s2;
     }
     named_bar(1, 128);
     if (q == 0 && lane < BN) {  // fixed order over the 4 lane quarters
-      const float tot = es->sq[0 * BN + lane] + es->sq[1 * BN + lane] + es->sq[2 * BN + lane] + es->sq[3 * BN + lane];
+      const float tot = et->sq[0 * BN + lane] + et->sq[1 * BN + lane] + et->sq[2 * BN + lane] + et->sq[3 * BN + lane];
       __stcg(ph.ssp_out + (size_t)lane * (a.d / BM) + t, lane < rows ? tot : 0.f);
     }
   } else if (ph.epi == kEpGateUp) {
     // lanes 0..63: gate rows, 64..127: up rows of the same 64 features
     if (nl >= 64) {
 #pragma unroll
-      for (int r = 0; r < BN; ++r) es->xchg[(nl - 64) * BN + r] = v[r];
+      for (int r = 0; r < BN; ++r) et->xchg[(nl - 64) * BN + r] = v[r];
     }
     named_bar(1, 128);
     if (nl < 64) {
@@ -286,7 +290,7 @@ AMUSD_DEV void tile_epilogue(const FwArgs& a, const GemmKind& ph, const __nv_bfl
 #pragma unroll
       for (int r = 0; r < BN; ++r) {
         if (r < rows) {
-          const float g = v[r] * inv[r], u = es->xchg[nl * BN + r] * inv[r];
+          const float g = v[r] * inv[r], u = et->xchg[nl * BN + r] * inv[r];
           ph.out_b[(size_t)r * ph.ldo + f] = __float2bfloat16((g / (1.f + expf(-g))) * u);
         }
       }
@@ -299,12 +303,12 @@ AMUSD_DEV void tile_epilogue(const FwArgs& a, const GemmKind& ph, const __nv_bfl
       if (a.logits && n < ph.N && r < rows) a.logits[(size_t)r * ph.N + n] = v[r] * inv[r];
       unsigned long long key = (valid_n && r < rows) ? argmax_key(v[r] * inv[r], n) : 0ull;
       key = warp_max_u64(key);
-      if (lane == 0) es->kx[q * BN + r] = key;
+      if (lane == 0) et->kx[q * BN + r] = key;
     }
     named_bar(1, 128);
     if (q == 0 && lane < BN && lane < rows) {
-      unsigned long long b = es->kx[lane];
-      for (int w = 1; w < 4; ++w) b = es->kx[w * BN + lane] > b ? es->kx[w * BN + lane] : b;
+      unsigned long long b = et->kx[lane];
+      for (int w = 1; w < 4; ++w) b = et->kx[w * BN + lane] > b ? et->kx[w * BN + lane] : b;
       atomicMax(a.best + lane, b);
     }
   }
@@ -1022,6 +1026,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
     const int q = warp & 3;        // TMEM lane quarter this warp may access
     const int nl = q * 32 + lane;  // tile row held by this thread
     EpiSmem* es = (EpiSmem*)(scratch + kAttnBytes);  // never aliased by the attention scratch
+    EpiTmp* et = (EpiTmp*)&((AttnSmem<HD, G>*)scratch)->kb[0][0];  // per item: aliases the K staging
+    static_assert(sizeof(EpiTmp) <= sizeof(((AttnSmem<HD, G>*)nullptr)->kb), "EpiTmp alias");
     if (tid == 0) es->inv_phase = -1;
     int n = 0, seg = 0, attn_dep_ok = -1;
     uint32_t attn_par = 0;
@@ -1139,7 +1145,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         }
         if (final) {
           const __nv_bfloat16* gnext = g.gnext ? g.gnext + (size_t)layer * g.gnext_stride : nullptr;
-          tile_epilogue(a, g, gnext, t, nl, acc, L.rows, es, q, lane);
+          tile_epilogue(a, g, gnext, t, nl, acc, L.rows, es, et, q, lane);
         }
         wrote = final;
         lm_last_check = epi == kEpArgmax;

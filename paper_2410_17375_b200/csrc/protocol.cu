@@ -108,11 +108,13 @@ __global__ void k_draft_begin(ProtoArgs a) {
       s->pred_valid = 0;
       coin_push(a.coin, target - 1, corr);
       mb_D(R)[target - 1 - a.P] = corr;    // D.truncate_to + append(c)
+      // stamp before publishing: the peer may act on the ack at once, and the merged
+      // trace orders events by these stamps
+      const long long now = globaltimer();
       st_release(&R->db.p_d, target);      // p_d = target
       R->db.acks += 1;
       c->rb_ack_local = req;
       st_release(&R->db.rb_ack, req);      // clear the request (epoch)
-      const long long now = globaltimer();
       trace_push(a.dtrace, now, now - c->t0, 3, target, pd, 0);
       continue;
     }
@@ -153,9 +155,9 @@ __global__ void k_draft_end(ProtoArgs a) {
   s->len = n + 1;
   s->pred_valid = 0;
   mb_D(R)[n - a.P] = tok;
+  const long long now = globaltimer();  // stamp before publishing (trace order)
   st_release(&R->db.p_d, n + 1);
   R->db.drafted += 1;
-  const long long now = globaltimer();
   trace_push(a.dtrace, now, now - c->t0, 0, n + 1, n + 1, 0);
 }
 
@@ -236,6 +238,7 @@ __global__ void k_verify_end(ProtoArgs a) {
   s->len = pv;
   s->kv_len = pv - 1;
   s->pred_valid = 0;
+  const long long now = globaltimer();  // stamp before publishing (trace order)
   mb_write_both(&R->vb.p_v, &L->vb.p_v, pv);
   R->vb.verify_steps += 1;
   if (L != R) L->vb.verify_steps = R->vb.verify_steps;
@@ -248,7 +251,6 @@ __global__ void k_verify_end(ProtoArgs a) {
     c->rb_ack_local += 1;
     mb_write_both(&R->vb.rb_req, &L->vb.rb_req, c->rb_ack_local);
   }
-  const long long now = globaltimer();
   trace_push(a.vtrace, now, now - c->t0, miss >= 0 ? 2 : 1, pv0 + 1, pv, miss >= 0 ? miss : m);
   if (eos_hit || pv - a.P >= a.N) {
     mb_write_both(&R->vb.complete, &L->vb.complete, 1);
