@@ -235,12 +235,20 @@ AMUSD_DEV GemmRes resolve(const FwArgs& a, int gk, int layer) {
 }
 
 // ------------------------------------------------------------ epilogues
-// Per-item epilogue temporaries: alias the attention K staging buffer (both belong to the
+// 4-byte asynchronous global -> shared copy (L2 only: the data was written by other CTAs)
+AMUSD_DEV void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+AMUSD_DEV void cp_async_wait_all() { asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory"); }
+
+// Per-item epilogue temporaries: alias the attention K/V staging buffers (both belong to the
 // epilogue warps, which run one item at a time; the attention mbarrier stays outside).
 struct EpiTmp {
   float xchg[64 * BN];                // gate/up exchange
   unsigned long long kx[4 * BN];      // argmax per lane-quarter
   float sq[4 * BN];                   // residual sum-of-squares per lane-quarter
+  float hs[BN][BM];                   // residual epilogue: the tile's h rows, prefetched (cp.async)
+  __nv_bfloat16 gs[BM];               // ... and the tile's slice of the next RMSNorm weight
 };
 // Epilogue state that persists across items (the RMSNorm scale of the current phase).
 struct EpiSmem {
@@ -251,6 +259,17 @@ struct EpiSmem {
 // Final epilogue of one 128-row tile; thread holds tile row nl, v[r] for the
 // 16 token rows.  Activations written here are read by other CTAs of the same
 // launch: all loads/stores bypass L1 (.cg).
+// Residual epilogue inputs of tile t: this thread's h column for every live row -> et->hs
+// (asynchronous; consumed by tile_epilogue after cp_async_wait_all, by the same thread).
+// The caller waits (cp_async_wait_all) before the CTA barrier that precedes tile_epilogue.
+AMUSD_DEV void resid_prefetch(const GemmKind& ph, const __nv_bfloat16* gnext, int t, int nl, int rows, EpiTmp* et) {
+  const int n = t * BM + nl;
+  for (int r = 0; r < rows; ++r) cp_async4(&et->hs[r][nl], ph.out + (size_t)r * ph.ldo + n);
+  if (nl < BM / 8)  // 16 threads x 16 bytes: the tile's 128 norm weights
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&et->gs[nl * 8])),
+                 "l"(gnext + t * BM + nl * 8) : "memory");
+}
+
 AMUSD_DEV void tile_epilogue(const FwArgs& a, const GemmKind& ph, const __nv_bfloat16* gnext, int t, int nl,
                              const float (&v)[BN], int rows, EpiSmem* es, EpiTmp* et, int q, int lane) {
   const float* inv = es->inv;
@@ -259,19 +278,20 @@ AMUSD_DEV void tile_epilogue(const FwArgs& a, const GemmKind& ph, const __nv_bfl
 #pragma unroll
     for (int r = 0; r < BN; ++r)
       if (r < rows) __stcg(ph.out + (size_t)r * ph.ldo + n, v[r] * inv[r]);
-  } else if (ph.epi == kEpResid) {
+  } else if (ph.epi == kEpResid) {  // h rows and norm weights prefetched by resid_prefetch
     const int n = t * BM + nl;
-    const float gn = __bfloat162float(gnext[n]);
+    const float gn = __bfloat162float(et->gs[nl]);
+    // live rows only (`rows` is uniform across the launch): the shuffle trees of the 16-row
+    // tile cost ~1.2 us on the merger's critical path
 #pragma unroll
     for (int r = 0; r < BN; ++r) {
-      float hn = 0.f;
       if (r < rows) {
-        hn = __ldcg(ph.out + (size_t)r * ph.ldo + n) + v[r];
+        const float hn = et->hs[r][nl] + v[r];
         __stcg(ph.out + (size_t)r * ph.ldo + n, hn);
         ph.xnext[(size_t)r * ph.ldo + n] = __float2bfloat16(hn * gn);
+        const float s2 = warp_sum(hn * hn);
+        if (lane == 0) et->sq[q * BN + r] = s2;
       }
-      const float s2 = warp_sum(hn * hn);
-      if (lane == 0) et->sq[q * BN + r] = s2;
     }
     named_bar(1, 128);
     if (q == 0 && lane < BN) {  // fixed order over the 4 lane quarters
@@ -300,10 +320,12 @@ AMUSD_DEV void tile_epilogue(const FwArgs& a, const GemmKind& ph, const __nv_bfl
     const bool valid_n = n < ph.N && !(a.exclude_eos && n == a.eos);
 #pragma unroll
     for (int r = 0; r < BN; ++r) {
-      if (a.logits && n < ph.N && r < rows) a.logits[(size_t)r * ph.N + n] = v[r] * inv[r];
-      unsigned long long key = (valid_n && r < rows) ? argmax_key(v[r] * inv[r], n) : 0ull;
-      key = warp_max_u64(key);
-      if (lane == 0) et->kx[q * BN + r] = key;
+      if (r < rows) {  // live rows only (uniform)
+        if (a.logits && n < ph.N) a.logits[(size_t)r * ph.N + n] = v[r] * inv[r];
+        unsigned long long key = valid_n ? argmax_key(v[r] * inv[r], n) : 0ull;
+        key = warp_max_u64(key);
+        if (lane == 0) et->kx[q * BN + r] = key;
+      }
     }
     named_bar(1, 128);
     if (q == 0 && lane < BN && lane < rows) {
@@ -1026,8 +1048,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
     const int q = warp & 3;        // TMEM lane quarter this warp may access
     const int nl = q * 32 + lane;  // tile row held by this thread
     EpiSmem* es = (EpiSmem*)(scratch + kAttnBytes);  // never aliased by the attention scratch
-    EpiTmp* et = (EpiTmp*)&((AttnSmem<HD, G>*)scratch)->kb[0][0];  // per item: aliases the K staging
-    static_assert(sizeof(EpiTmp) <= sizeof(((AttnSmem<HD, G>*)nullptr)->kb), "EpiTmp alias");
+    EpiTmp* et = (EpiTmp*)&((AttnSmem<HD, G>*)scratch)->kb[0][0];  // per item: aliases the K/V staging
+    static_assert(sizeof(EpiTmp) <= 2 * sizeof(((AttnSmem<HD, G>*)nullptr)->kb), "EpiTmp alias");
+    using AS = AttnSmem<HD, G>;
+    static_assert(offsetof(AS, vb) == sizeof(((AS*)nullptr)->kb), "kb|vb contiguous");
     if (tid == 0) es->inv_phase = -1;
     int n = 0, seg = 0, attn_dep_ok = -1;
     uint32_t attn_par = 0;
@@ -1124,6 +1148,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
               else red_add_release(a.tile_cnt + g.cnt_off + t * kPad, 1);
             }
           } else {
+            // the residual rows and the next norm weight are final since earlier phases:
+            // fetch them while the chunk count is awaited
+            const __nv_bfloat16* gnext = g.gnext ? g.gnext + (size_t)layer * g.gnext_stride : nullptr;
+            if (epi == kEpResid) {
+              resid_prefetch(g, gnext, t, nl, L.rows, et);
+              cp_async_wait_all();  // (lands while tid 0 awaits the count; others wait at the barrier)
+            }
             if (tid == 0) {
               wait_count(a.tile_cnt + g.cnt_off + t * kPad, nchunks - 1);
               a.tile_cnt[g.cnt_off + t * kPad] = 0;  // re-arm for the next phase / launch
@@ -1140,6 +1171,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
             }
           }
         } else {
+          if (epi == kEpResid) {
+            resid_prefetch(g, g.gnext + (size_t)layer * g.gnext_stride, t, nl, L.rows, et);
+            cp_async_wait_all();
+            named_bar(1, 128);
+          }
 #pragma unroll
           for (int r = 0; r < BN; ++r) acc[r] = v[r];
         }
