@@ -1133,10 +1133,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
           // tile is bit-identical whatever the chunks' arrival order (deterministic, batch
           // invariant) and no partial ever needs a merge round trip.  Layout [tile][row][128].
           unsigned long long* acc64 = (unsigned long long*)a.ws + g.ws_off + (size_t)t * BN * BM + nl;
+          // live rows only: dead rows' accumulators are never added, read or re-armed
 #pragma unroll
           for (int r = 0; r < BN; ++r) {
-            const long long fx = __float2ll_rn(v[r] * 4294967296.0f);
-            asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(acc64 + r * BM), "l"(fx) : "memory");
+            if (r < L.rows) {
+              const long long fx = __float2ll_rn(v[r] * 4294967296.0f);
+              asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(acc64 + r * BM), "l"(fx) : "memory");
+            }
           }
           named_bar(1, 128);
           // The tile's last chunk (grabbed after its other chunks) merges; the others publish
@@ -1163,11 +1166,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
             named_bar(1, 128);
             long long s64[BN];
 #pragma unroll
-            for (int r = 0; r < BN; ++r) s64[r] = (long long)__ldcg(acc64 + r * BM);
+            for (int r = 0; r < BN; ++r) s64[r] = r < L.rows ? (long long)__ldcg(acc64 + r * BM) : 0ll;
 #pragma unroll
             for (int r = 0; r < BN; ++r) {
               acc[r] = (float)((double)s64[r] * (1.0 / 4294967296.0));
-              __stcg(acc64 + r * BM, 0ull);  // re-arm the accumulator (next use is a later phase)
+              if (r < L.rows) __stcg(acc64 + r * BM, 0ull);  // re-arm (next use is a later phase)
             }
           }
         } else {
