@@ -1088,9 +1088,12 @@ __global__ void __launch_bounds__(kThreads, MINB)
         mbar_arrive(smem_u32(&tempty[b]));
         ++seg;
         const int epi = g.epi, nchunks = g.nchunks;
-        // RMSNorm scale of the phase's input rows (once per phase per CTA)
+        // RMSNorm scale of the phase's input rows (once per phase per CTA).  Only the merging
+        // item scales (the scale is linear and applies to the exact sum): contributors skip
+        // this round trip and publish at once.
         const bool need_inv = epi == kEpStoreScaled || epi == kEpGateUp || epi == kEpArgmax;
-        if (need_inv && es->inv_phase != p) {
+        const bool final_item = nchunks <= 1 || j / g.ntiles == nchunks - 1;
+        if (need_inv && final_item && es->inv_phase != p) {
           // the RMSNorm scale needs the whole input row: wait for the full producer phase
           // (the MMA above only needed the tiles of its K range)
           if (a.fine) {  // (phase-level mode: the MMA already waited for the whole phase)
