@@ -118,6 +118,9 @@ struct amusd_model {
   int fw_part_grid = 0;             // ... built for this many SMs (0 = none yet)
   bool fw_part_ok = false;          // draft role only: split-K chunking changes the fp32 partials,
                                     // so the verify keeps one chunking in every engine (AR parity)
+  const int* fw_ab_req = nullptr;   // draft cut words (set while capturing the AMUSD draft loop)
+  const int* fw_ab_done = nullptr;
+  size_t fw_ws_floats = 0, fw_cnt_ints = 0, fw_attn_cnt_ints = 0;  // cut cleanup extents
   int grid_override = 0;            // amusd_model_set_grid: SMs of amusd_time_forward launches (0 = all)
   int path = AMUSD_PATH_PERSISTENT;
   long long* fw_dbg = nullptr;  // optional per-item timeline (amusd_model_set_timeline)
@@ -248,6 +251,14 @@ static size_t tf_carve(const amusd_tf_config* c, void* base, amusd_model* m) {
     m->attn_ws = attn_ws; m->attn_cnt = attn_cnt;
     m->fw_sched = fsched; m->fw_best = fbest; m->fw_ws = fws; m->fw_tile_cnt = fcnt; m->fw_norms = fnorms;
     m->fw_attn_ws = fattn_ws; m->fw_attn_cnt = fattn_cnt;
+    if (tc) {
+      size_t wsf;
+      int cints, mt;
+      fw_sizes(c, &wsf, &cints, &mt);
+      m->fw_ws_floats = std::max<size_t>(wsf, 1);
+      m->fw_cnt_ints = (size_t)cints;
+      m->fw_attn_cnt_ints = (size_t)c->n_kv_heads * KMAX * fw::kCounterInts;
+    }
     m->fw_xb = fxb; m->fw_sspb = fsspb; m->fw_tflag = ftflag; m->fw_agrp = fagrp;
     m->tc = tc; m->xa_b = xa_b; m->attn_b = attn_b; m->act_b = act_b; m->inv = inv; m->ssp = ssp_b; m->tc_ws = ws; m->tc_cnt = cnt; m->tiled = tiled;
     m->seq = seq; m->tok = tok; m->api_ctl = ctl; m->kc = kc; m->vc = vc; m->h = h; m->qkv = qkv;
@@ -425,6 +436,7 @@ static int fw_forward(amusd_model* m, StepCtl* ctl, cudaStream_t st, bool want_l
   a.max_splits = fw::attn_splits(c.max_seq); a.vocab = c.vocab; a.eos = c.eos_token; a.exclude_eos = c.exclude_eos;
   a.scale = 1.0f / sqrtf((float)c.head_dim); a.eps = c.norm_eps;
   a.dbg = m->fw_dbg; a.dbg_items = m->fw_dbg_items;
+  a.ab_req = m->fw_ab_req; a.ab_done = m->fw_ab_done;
   // L2 prefetch window (bytes of weights ahead of the grab pointer), AMUSD_FW_L2_MB
   a.prefetch_items = (int)((size_t)env_int("AMUSD_FW_L2_MB", 0) * (1 << 20) / ((size_t)fw_units() * 16384));
   a.inflight = env_int("AMUSD_FW_INFLIGHT", 0);
@@ -432,6 +444,9 @@ static int fw_forward(amusd_model* m, StepCtl* ctl, cudaStream_t st, bool want_l
   a.debug = env_int("AMUSD_FW_DEBUG", 0);
   a.fine = env_int("AMUSD_FW_FINE", 0);  // per-tile deps measured slower: CTAs run their queues in order
   CUDA_TRY(fw::launch_forward(a, m->map_xa, m->map_attn, m->map_act, m->map_xb, m->fw_grid, m->fw_stages, st));
+  if (a.ab_req)
+    CUDA_TRY(fw::launch_cut_cleanup(m->fw_sched, m->fw_ws, m->fw_ws_floats, m->fw_tile_cnt, m->fw_cnt_ints,
+                                    m->fw_attn_cnt, m->fw_attn_cnt_ints, m->fw_best, st));
   return AMUSD_OK;
 }
 
@@ -999,7 +1014,14 @@ static int capture_body(amusd_session* s, int engine, int actor, cudaGraph_t bod
     }
     pk(kSyncVerifyBegin, 0); fwd(s->verify, s->vctl, KMAX); pk(kSyncVerifyEnd, 0);
   } else if (actor == 0) {
+    // a rollback request or completion raised during the draft forward discards its token
+    // (k_draft_end): cut the forward short (AMUSD_FW_CUT=0 disables)
+    if (env_int("AMUSD_FW_CUT", 1)) {
+      s->draft->fw_ab_req = &s->mb_local->vb.rb_req;
+      s->draft->fw_ab_done = &s->mb_local->vb.complete;
+    }
     pk(kDraftBegin, 0); fwd(s->draft, s->dctl, 2); pk(kDraftEnd, 0);
+    s->draft->fw_ab_req = s->draft->fw_ab_done = nullptr;
   } else {
     pk(kVerifyBegin, 0); fwd(s->verify, s->vctl, KMAX); pk(kVerifyEnd, 0);
   }

@@ -53,6 +53,7 @@ constexpr int kWarpX = 1, kWarpMma0 = 2, kWarpEpi0 = 6;
 constexpr int kTbuf = 4;                 // TMEM accumulator buffers (MMA may run 3 items ahead of the epilogue)
 constexpr int kTmemCols = kTbuf * NACC * BN;  // 256
 constexpr int kMaxMerge = 128;         // max position splits of one row (8192 positions)
+constexpr int kCutIndex = 1 << 28;     // grab counter value after a draft cut (> any item count)
 constexpr int kAttnChunk = 64;         // positions per attention split (K/V chunk staged in smem; 2 threads each)
 constexpr long long kWaitNs = 4ll * 1000 * 1000 * 1000;  // dependency waits trap after 4 s
 // Every schedule counter owns a 128-byte line (grab counter, exit counter, one
@@ -871,6 +872,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
       }
       if (ahead > 0)  // the first `ahead` items have no earlier grabber: spread them over the CTAs
         for (int k = blockIdx.x; k < ahead; k += gridDim.x) prefetch_item(k);
+      // draft cut probe: loaded with each grab, consumed at the next (never blocks the stream)
+      const int ab_ack = a.ab_req ? ld_volatile(&a.ctl->rb_ack_local) : 0;
+      auto ab_probe = [&]() { return a.ab_req ? (ld_volatile(a.ab_req) ^ ab_ack) | ld_volatile(a.ab_done) : 0; };
+      bool cut = false;
+      int ab_next = ab_probe();
       int i_next = atomicAdd(a.sched, 1);  // grab counter: sched[0]; exit counter: sched[kPad]
       // Attention items go to drained CTAs: grabbed eagerly behind a GEMM still in flight, an
       // attention item (and its row's split merge) would wait for that GEMM's whole epilogue.
@@ -880,11 +886,17 @@ __global__ void __launch_bounds__(kThreads, MINB)
         // (only QKV and attention items can be followed by an attention grab: the others
         // grab eagerly, without the peek's round trip)
         const int i = i_next;
+        if (ab_next && !cut) {  // cut: no item beyond the grabbed prefix is handed out
+          cut = true;
+          atomicMax(a.sched, kCutIndex);
+          atomicExch(a.sched + 2 * kPad + 1, 1);  // launch_cut_cleanup flag
+        }
         bool have_next = false;
         if (i < L.total) {
           const int k = kind_of(locate(a, L, i).x, a.L);
           if (k != kKQkv && k != kKAttn) {
             i_next = atomicAdd(a.sched, 1);
+            if (!cut) ab_next = ab_probe();
             have_next = true;
           }
         }
@@ -943,6 +955,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
             __nanosleep(64);
           }
           i_next = atomicAdd(a.sched, 1);
+          if (!cut) ab_next = ab_probe();
         }
       }
     }
@@ -1285,6 +1298,28 @@ __global__ void __launch_bounds__(kThreads, MINB)
       __threadfence();
     }
   }
+}
+
+__global__ void __launch_bounds__(1024) k_cut_cleanup(int* flag, float* ws, size_t ws_floats, int* tile_cnt,
+                                                      size_t cnt_ints, int* attn_cnt, size_t attn_cnt_ints,
+                                                      unsigned long long* best) {
+  if (ld_volatile(flag) == 0) return;  // not cut: nothing to re-arm
+  uint4* w = (uint4*)ws;               // (16-byte aligned carve; ws_floats is even)
+  const size_t nw = ws_floats / 4;
+  for (size_t i = threadIdx.x; i < nw; i += blockDim.x) w[i] = make_uint4(0, 0, 0, 0);
+  for (size_t i = nw * 4 + threadIdx.x; i < ws_floats; i += blockDim.x) ws[i] = 0.f;
+  for (size_t i = threadIdx.x; i < cnt_ints; i += blockDim.x) tile_cnt[i] = 0;
+  for (size_t i = threadIdx.x; i < attn_cnt_ints; i += blockDim.x) attn_cnt[i] = 0;
+  if (threadIdx.x < KMAX) best[threadIdx.x] = 0ull;
+  __syncthreads();
+  if (threadIdx.x == 0) *flag = 0;
+}
+
+cudaError_t launch_cut_cleanup(int* sched, float* ws, size_t ws_floats, int* tile_cnt, size_t cnt_ints,
+                               int* attn_cnt, size_t attn_cnt_ints, unsigned long long* best, cudaStream_t st) {
+  k_cut_cleanup<<<1, 1024, 0, st>>>(sched + 2 * kPad + 1, ws, ws_floats, tile_cnt, cnt_ints, attn_cnt, attn_cnt_ints,
+                                    best);
+  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------ host side

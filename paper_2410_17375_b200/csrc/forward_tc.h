@@ -79,6 +79,13 @@ struct FwArgs {
   int inflight;                 // max unlanded weight units per CTA (0 = ring depth)
   int debug;                    // perf-isolation bits (AMUSD_FW_DEBUG), 0 in production
   int fine;                     // 1: per-tile dependencies (AMUSD_FW_FINE); 0: phase-level (default)
+  // Draft cut (co-located / split AMUSD draft only, else null): once the verifier has raised
+  // a rollback request (*ab_req != ctl->rb_ack_local) or completion (*ab_done), this forward's
+  // token will be discarded (k_draft_end), so the grab counter is moved past the item list.
+  // Grabs are in index order and every wait targets lower indices, so the grabbed prefix
+  // drains normally; launch_cut_cleanup re-arms the split state a cut tile/row left behind.
+  const int* ab_req;
+  const int* ab_done;
   long long* dbg;               // optional per-item timeline [item][8] (perf analysis), null in production
   int dbg_items;
 };
@@ -114,7 +121,11 @@ void build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_f
 
 cudaError_t launch_forward(const FwArgs& a, const CUtensorMap& m_xa, const CUtensorMap& m_attn,
                            const CUtensorMap& m_act, const CUtensorMap& m_xb, int grid, int stages, cudaStream_t st);
-// schedule counters: grab, exit, epoch, then one per phase (kCounterInts each)
+// After a forward launched with ab_req: if it was cut (flag in the schedule), zero the split-K
+// accumulators / counters, attention counters and argmax keys (one CTA; a no-op otherwise).
+cudaError_t launch_cut_cleanup(int* sched, float* ws, size_t ws_floats, int* tile_cnt, size_t cnt_ints,
+                               int* attn_cnt, size_t attn_cnt_ints, unsigned long long* best, cudaStream_t st);
+// schedule counters: grab, exit, epoch (+ cut flag), then one per phase (kCounterInts each)
 inline size_t sched_ints(int L) { return (size_t)(3 + num_phases(L)) * kCounterInts; }
 int forward_smem_bytes(int stages, int hd, int group);
 
