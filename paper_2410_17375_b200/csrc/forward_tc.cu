@@ -59,7 +59,10 @@ constexpr long long kWaitNs = 4ll * 1000 * 1000 * 1000;  // dependency waits tra
 // Every schedule counter owns a 128-byte line (grab counter, exit counter, one
 // per phase, one per split-K tile): 148 CTAs poll and bump them concurrently.
 constexpr int kPad = kCounterInts;
-constexpr unsigned a_poll_ns = 100;
+#ifndef AMUSD_POLL_NS
+#define AMUSD_POLL_NS 100
+#endif
+constexpr unsigned a_poll_ns = AMUSD_POLL_NS;  // dependency-poll back-off (ns)
 constexpr unsigned kSuspendNs = 20000;  // mbarrier try_wait suspend-time hint
 
 // ------------------------------------------------------------ memory model
