@@ -167,7 +167,7 @@ static bool tc_shapes_ok(const amusd_tf_config* c) {
   // and a QKV group block [q(G heads) | k | v] spans whole 128-row tiles
   const int G = c->n_kv_heads ? c->n_heads / c->n_kv_heads : 0;
   return c->dtype == AMUSD_BF16 && c->use_tensor_cores && c->d_model % 128 == 0 && ncols % 128 == 0 &&
-         c->ffn % 64 == 0 && c->vocab % 128 == 0 && (c->n_heads * c->head_dim) % 64 == 0 &&
+         c->ffn % 128 == 0 && c->vocab % 128 == 0 && (c->n_heads * c->head_dim) % 128 == 0 &&
          ((G + 2) * c->head_dim) % 128 == 0;
 }
 

@@ -48,6 +48,13 @@ namespace fw {
 using namespace amusd::tc;
 
 constexpr int kQ = 4;                  // item queue depth
+// Units (16 KB weight tile + 2 KB token tile) per ring stage: one full/empty handshake and one
+// commit per stage.  The handshake (~200 cycles, tools/probe/probe_ring.cu) plus the MMA issue
+// per 16 KB capped a CTA at ~45 GB/s with 1 unit per stage; a bare bulk-copy ring streams
+// ~200 GB/s per SM (tools/probe/probe_bw.cu).
+constexpr int kUPS = 2;
+constexpr int kStageW = kUPS * kWBytes;
+constexpr int kStageX = kUPS * kXBytes;
 constexpr int kThreads = 320;
 constexpr int kWarpX = 1, kWarpMma0 = 2, kWarpEpi0 = 6;
 constexpr int kTbuf = 4;                 // TMEM accumulator buffers (MMA may run 3 items ahead of the epilogue)
@@ -776,8 +783,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int S = a.stages;
   uint8_t* sW = smem;
-  uint8_t* sX = smem + S * kWBytes;
-  uint8_t* scratch = sX + S * kXBytes;  // attention scratch / epilogue exchange (epilogue warps only)
+  uint8_t* sX = smem + S * kStageW;
+  uint8_t* scratch = sX + S * kStageX;  // attention scratch / epilogue exchange (epilogue warps only)
   constexpr int kAttnBytes = attn_scratch_bytes<HD, G>();
   constexpr int kScratch = kAttnBytes + epi_bytes();
   uint64_t* bars = (uint64_t*)(scratch + kScratch);
@@ -931,10 +938,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
           const GemmRes g = resolve(a, gemm_of(kind), layer_of(pj.x));
           const int c = pj.y / g.ntiles, t = pj.y - c * g.ntiles;  // chunk-major item order
           const uint8_t* src = g.wt + ((size_t)t * g.kb + (size_t)c * g.kc) * kWBytes;
-          for (int u = 0; u < g.kc; ++u, ++gu, rg.next(S)) {
+          for (int u = 0; u < g.kc; u += kUPS, ++gu, rg.next(S)) {  // (kc % kUPS == 0: build_kinds)
             const int s = rg.s;
             mbar_wait_t(smem_u32(&empty[s]), rg.ph ^ 1u);
-            // Optional outstanding-load cap (AMUSD_FW_INFLIGHT): at most `inflight` unlanded units.
+            // Optional outstanding-load cap (AMUSD_FW_INFLIGHT): at most `inflight` unlanded stages.
             if (inflight < S && gu >= inflight) {
               mbar_wait_t(smem_u32(&wfull[rl.s]), rl.ph);
               rl.next(S);
@@ -943,11 +950,16 @@ __global__ void __launch_bounds__(kThreads, MINB)
               mbar_arrive(smem_u32(&wfull[s]));
               continue;
             }
-            mbar_expect_tx(smem_u32(&wfull[s]), kWBytes);
-            if (a.debug & 16)  // perf knob: no L2 eviction hint on the weight stream
-              bulk_load_nohint(smem_u32(sW + s * kWBytes), src + (size_t)u * kWBytes, kWBytes, smem_u32(&wfull[s]));
-            else
-              bulk_load(smem_u32(sW + s * kWBytes), src + (size_t)u * kWBytes, kWBytes, smem_u32(&wfull[s]), pol_w);
+            mbar_expect_tx(smem_u32(&wfull[s]), kStageW);
+#pragma unroll
+            for (int uu = 0; uu < kUPS; ++uu) {
+              const uint32_t dst = smem_u32(sW + s * kStageW + uu * kWBytes);
+              const uint8_t* from = src + (size_t)(u + uu) * kWBytes;
+              if (a.debug & 16)  // perf knob: no L2 eviction hint on the weight stream
+                bulk_load_nohint(dst, from, kWBytes, smem_u32(&wfull[s]));
+              else
+                bulk_load(dst, from, kWBytes, smem_u32(&wfull[s]), pol_w);
+            }
           }
           dbg_mark(a, i, 2, globaltimer());
         }
@@ -1006,15 +1018,18 @@ __global__ void __launch_bounds__(kThreads, MINB)
         }
         if (a.dbg) dbg_mark(a, phase_first(a, L, it.x) + it.y, 3, globaltimer());
         const CUtensorMap* map = g.map == 0 ? &m_xa : (g.map == 1 ? &m_attn : (g.map == 2 ? &m_act : &m_xb));
-        for (int u = 0; u < kc; ++u, rg.next(S)) {
+        for (int u = 0; u < kc; u += kUPS, rg.next(S)) {
           const int s = rg.s;
           mbar_wait_t(smem_u32(&empty[s]), rg.ph ^ 1u);
           if (a.debug & 4) {  // perf isolation: no activation traffic
             mbar_arrive(smem_u32(&xfull[s]));
             continue;
           }
-          mbar_expect_tx(smem_u32(&xfull[s]), kXBytes);
-          tma_load_2d(smem_u32(sX + s * kXBytes), map, (c * kc + u) * BK, 0, smem_u32(&xfull[s]), pol_x);
+          mbar_expect_tx(smem_u32(&xfull[s]), kStageX);
+#pragma unroll
+          for (int uu = 0; uu < kUPS; ++uu)
+            tma_load_2d(smem_u32(sX + s * kStageX + uu * kXBytes), map, (c * kc + u + uu) * BK, 0,
+                        smem_u32(&xfull[s]), pol_x);
         }
       }
     }
@@ -1039,7 +1054,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         mbar_wait_t(smem_u32(&tempty[b]), ((seg / kTbuf) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)((b * NACC + kk) * BN);
-        for (int u = 0; u < kc; ++u, rg.next(S)) {
+        for (int u = 0; u < kc; u += kUPS, rg.next(S)) {
           const int s = rg.s;
           const uint32_t par = rg.ph;
           mbar_wait_t(smem_u32(&wfull[s]), par);
@@ -1049,9 +1064,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
             mbar_arrive(smem_u32(&empty[s]));
             continue;
           }
-          umma(d, umma_desc(smem_u32(sW + s * kWBytes) + kk * 32), umma_desc(smem_u32(sX + s * kXBytes) + kk * 32),
-               u > 0 ? 1u : 0u);
-          umma_commit(smem_u32(&empty[s]));
+#pragma unroll
+          for (int uu = 0; uu < kUPS; ++uu)
+            umma(d, umma_desc(smem_u32(sW + s * kStageW + uu * kWBytes) + kk * 32),
+                 umma_desc(smem_u32(sX + s * kStageX + uu * kXBytes) + kk * 32), (u + uu) > 0 ? 1u : 0u);
+          umma_commit(smem_u32(&empty[s]));  // one commit per stage
         }
         if (nomma) mbar_arrive(smem_u32(&tfull[b]));
         else umma_commit(smem_u32(&tfull[b]));
@@ -1103,6 +1120,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         tc_fence_before();
         mbar_arrive(smem_u32(&tempty[b]));
         ++seg;
+        if (a.dbg && tid == 0 && v[0] != 12345.f) dbg_mark(a, phase_first(a, L, p) + j, 6, globaltimer());  // TEMP tmem read
         const int epi = g.epi, nchunks = g.nchunks;
         // RMSNorm scale of the phase's input rows (once per phase per CTA).  Only the merging
         // item scales (the scale is linear and applies to the exact sum): contributors skip
@@ -1165,6 +1183,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           // with a fire-and-forget release and move on -- no round trip in their epilogue.
           final = cj == nchunks - 1;
           if (!final) {
+            if (a.dbg && tid == 0) dbg_mark(a, phase_first(a, L, p) + j, 2, globaltimer());  // TEMP reds+bar done
             if (tid == 0) {
               if (a.debug & 32) red_add_relaxed(a.tile_cnt + g.cnt_off + t * kPad, 1);  // timing experiment only
               else red_add_release(a.tile_cnt + g.cnt_off + t * kPad, 1);
@@ -1330,10 +1349,12 @@ int attn_items_max(int KV, int S) { return KV * KMAX * attn_splits(S); }
 int attn_splits(int S) { return (S + kAttnChunk - 1) / kAttnChunk; }
 int max_positions() { return kMaxMerge * kAttnChunk; }
 
+// Units per item: the largest divisor of kb that is <= target and a whole number of ring
+// stages (kb is even for every supported shape: tc_shapes_ok).
 static int pick_kc(int kb, int target) {
-  int best = 1;
-  for (int k = 1; k <= kb; ++k)
-    if (kb % k == 0 && k <= target) best = k;
+  int best = kUPS;
+  for (int k = kUPS; k <= kb; k += kUPS)
+    if (kb % k == 0 && k <= std::max(target, kUPS)) best = k;
   return best;
 }
 
@@ -1422,7 +1443,7 @@ int forward_smem_bytes(int stages, int hd, int group) {
 #undef AMUSD_SC
   if (!sc) return 0;
   const int ctl = (3 * stages + 2 * kTbuf + 2 * kQ) * 8 + kQ * 8 + 4 + 5 * 4;
-  return 1024 + stages * (kWBytes + kXBytes) + sc + ((ctl + 127) & ~127);
+  return 1024 + stages * (kStageW + kStageX) + sc + ((ctl + 127) & ~127);
 }
 
 template <int HD, int G, int MINB>

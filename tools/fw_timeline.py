@@ -24,6 +24,7 @@ ap.add_argument("--layers", type=int, default=8)
 ap.add_argument("--rows", type=int, default=1)
 ap.add_argument("--pos", type=int, default=300)
 ap.add_argument("--out", default="gpurun_out/tl.npy")
+ap.add_argument("--grid", type=int, default=0, help="SMs of the persistent launch (0 = all)")
 a = ap.parse_args()
 TC = P.TransformerConfig
 kw = {"max_seq": 640}
@@ -36,6 +37,7 @@ lib = L.load()
 buf = torch.zeros(1 << 17, 8, dtype=torch.int64, device="cuda")
 L.check(lib.amusd_model_set_timeline(m.handle, C.c_void_p(buf.data_ptr()), buf.numel() * 8))
 ms = C.c_float()
+L.check(lib.amusd_model_set_grid(m.handle, a.grid))
 L.check(lib.amusd_time_forward(m.handle, a.rows, -1, 0, 3, C.byref(ms), device_stream(m.device)))
 torch.cuda.synchronize()
 t = buf.cpu().numpy()

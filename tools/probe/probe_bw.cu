@@ -78,5 +78,8 @@ int main() {
   BULK(16384, 5, false, 148) BULK(16384, 8, false, 148) BULK(16384, 12, false, 148) BULK(32768, 6, false, 148)
   BULK(16384, 5, false, 296) BULK(16384, 6, false, 296)
   BULK(16384, 5, true, 148) BULK(16384, 8, true, 148) BULK(16384, 12, true, 148)
+  // per-SM streaming rate at partial grids (the persistent forward's 10-stage ring)
+  BULK(16384, 10, false, 16) BULK(16384, 10, false, 32) BULK(16384, 10, false, 84) BULK(16384, 10, false, 148)
+  BULK(32768, 6, false, 16) BULK(65536, 3, false, 16)
   return 0;
 }
