@@ -1349,6 +1349,16 @@ int attn_items_max(int KV, int S) { return KV * KMAX * attn_splits(S); }
 int attn_splits(int S) { return (S + kAttnChunk - 1) / kAttnChunk; }
 int max_positions() { return kMaxMerge * kAttnChunk; }
 
+static int num_sms_host() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
 // Units per item: the largest divisor of kb that is <= target and a whole number of ring
 // stages (kb is even for every supported shape: tc_shapes_ok).
 static int pick_kc(int kb, int target) {
@@ -1380,7 +1390,15 @@ void build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_f
     // takes whole-K items (no split-K merge before the argmax) -- both measured best
     const bool chain = name[0] == 'Q' || (name[0] == 'O' && name[1] == 0);
     const bool lm = name[0] == 'L';
-    const int dflt = chain ? std::max(1, units_per_item / 2) : (lm ? 64 : units_per_item);
+    int dflt = chain ? std::max(1, units_per_item / 2) : (lm ? 64 : units_per_item);
+    if (!chain && !lm && units_per_item == 16) {
+      // gate/up and down: the largest of 32 / 16 / 8 units that still gives >= 1.5 items per
+      // SM (measured: 8B down 32, 1B down 8, gate/up 32 / 16 within noise)
+      const int sms = num_sms_host();
+      dflt = 8;
+      for (int u : {32, 16})
+        if (2 * ntiles * (g.kb / pick_kc(g.kb, u)) >= 3 * sms) { dflt = u; break; }
+    }
     const int want = kind_units(name, dflt);
     g.kc = pick_kc(g.kb, want);
     // A forward on a partial grid (co-located AMUSD draft) streams through fewer SMs: items
