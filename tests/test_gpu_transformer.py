@@ -146,6 +146,27 @@ def test_bf16_batch_invariance(bf16_pair):
             res.trace.validate()
 
 
+def test_amusd_draft_cut_on_and_off(bf16_pair, monkeypatch):
+    """AMUSD with the draft cut (a rollback raised mid-forward ends the draft forward at the
+    grabbed prefix; the split state is re-armed) and without it: tokens == AR, valid traces,
+    and the draft cut leaves no stale split-K state behind (a later AR run still matches)."""
+    d, v = bf16_pair
+    cfg = P.DecodeConfig(max_new_tokens=96)
+    ar = P.decode_autoregressive(v, PROMPT, cfg)
+    d_ar = P.decode_autoregressive(d, PROMPT, cfg).tokens  # before any cut forward
+    for cut in ("0", "1"):
+        monkeypatch.setenv("AMUSD_FW_CUT", cut)
+        P.engines.clear_sessions()  # the knob is read when the session's graphs are captured
+        for rho in (0.5, 0.8):
+            res = P.decode_speculative_async(P.AgreementDraft(d, rho), v, PROMPT, cfg)
+            assert res.tokens == ar.tokens, (cut, rho)
+            res.trace.validate()
+        # the draft model's own greedy decode after cut forwards: unchanged (no stale
+        # split-K accumulators / counters / argmax keys)
+        assert P.decode_autoregressive(d, PROMPT, cfg).tokens == d_ar, cut
+    P.engines.clear_sessions()
+
+
 def test_llama_shapes_run():
     """1B/8B-shaped bf16 pair (reduced N): kernels handle the real shapes; AMUSD == AR."""
     TC = P.TransformerConfig
