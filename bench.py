@@ -193,7 +193,7 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
         "amusd": (DeviceSession(draft, vm, Plen, cfg, canon=canon, max_window=args.window), L.ENGINE_ASYNC),
     }
     kd, kv = sess["amusd"][0].kernels_per_step(L.ENGINE_ASYNC)
-    _, kv_sync = sess["sync"][0].kernels_per_step(L.ENGINE_SYNC)
+    kd_sync, kv_sync = sess["sync"][0].kernels_per_step(L.ENGINE_SYNC)
     results, ref_tokens = {}, None
     sampler = None
     for name in ("ar", "sync", "amusd"):
@@ -219,7 +219,7 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
             if name == "ar":
                 launches += out.info.verify_iters * (kv - 2 + 2)
             elif name == "sync":
-                launches += out.info.verify_iters * (args.k * kd + kv_sync)
+                launches += out.info.verify_iters * (args.k * kd_sync + kv_sync)
             else:
                 launches += out.info.draft_iters * kd + out.info.verify_iters * kv
             stats.append(out.info)
@@ -255,8 +255,11 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
         L.check(lib.amusd_time_forward(m.handle, rows, which, layer, iters, C.byref(ms),
                                        torch.cuda.current_stream().cuda_stream))
         return ms.value
-    vm.init_state(prompt)
-    dm.init_state(prompt)
+    first_logits = {}
+    for key, m in (("verify", vm), ("draft", dm)):   # parity leg (cpu_leg): first-step logits
+        st = m.init_state(prompt)
+        m.next_token(st)
+        first_logits[key] = m.last_logits(1).numpy()[0]
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if peaks else "fallback"
@@ -305,85 +308,129 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "includes": "prefill of both models + graph launch + V/trace read-back + trace merge"}
     return {"results": results, "roofline": roofline, "e2e": e2e, "clocks": sampler.summary() if sampler else None,
-            "vm": vm, "dm": dm, "prompt": prompt, "canon": canon.tolist(), "vcfg": vcfg, "dcfg": dcfg}
+            "vm": vm, "dm": dm, "prompt": prompt, "canon": canon.tolist(), "vcfg": vcfg, "dcfg": dcfg,
+            "first_logits": first_logits}
 
 
 # --------------------------------------------------------------- CPU arm
-def cpu_models(vm, dm, vcfg, dcfg):
-    from oracle.ref_decoder import RefDecoder, TfShape
-
-    def mk(m, c):
-        shp = TfShape(c.vocab_size, c.d_model, c.n_layers, c.n_heads, c.n_kv_heads, c.head_dim, c.ffn,
-                      eos=c.eos_token, exclude_eos=c.exclude_eos, eps=c.norm_eps, theta=c.rope_theta, kv_bf16=True)
-        return RefDecoder(shp, m.host_weights(), tied=c.tied)
-    return mk(vm, vcfg), mk(dm, dcfg)
+def _shapes(args, max_seq):
+    from paper_2410_17375_b200.models import TransformerConfig as TC   # pure Python (no libamusd)
+    if args.shapes == "tiny":
+        return TC.tiny_verify(max_seq=max_seq), TC.tiny_draft(max_seq=max_seq)
+    return TC.llama_8b(max_seq=max_seq), TC.llama_1b(max_seq=max_seq)
 
 
-def cpu_sample(rv, rd, prompt, canon, rho, n_tokens: int) -> dict:
-    """Bounded CPU sample: reference AR and two-thread AMUSD on the numpy models."""
-    from oracle import specdec_oracle as O
-    from oracle.ref_decoder import CanonCoinDraft
-    cd = CanonCoinDraft(rd, canon, rho, 1234)
+def cpu_decoders(vcfg, dcfg, wv, wd):
+    """fp32 numpy decoders (oracle/ref_decoder.py) over bf16-valued weights, bf16 KV (as the GPU)."""
+    from oracle.ref_decoder import RefDecoder
+    from oracle.ref_models import shape_of
+    return (RefDecoder(shape_of(vcfg, kv_bf16=True), wv, tied=vcfg.tied),
+            RefDecoder(shape_of(dcfg, kv_bf16=True), wd, tied=dcfg.tied))
+
+
+def reference_cpu_run(rv, rd, prompt, rho, n_tokens, steps=1, warmup=0, k=4):
+    """The reference's OWN engines (unmodified specdec: decode_autoregressive and
+    decode_speculative_async with ThreadExecutor + the SURVEY section 0.6 trace shim,
+    engines.py:279-287, 409-561) driving the numpy decoders through the MockModel hooks
+    (oracle/ref_models.py).  Decode only is timed (the executor's wall time; prefill excluded).
+    Returns the CPU AR tokens (parity vs the GPU), AR and AMUSD tokens/s."""
+    from oracle.ref_models import load_reference, make_models
+    S = load_reference()
+    if S is None:
+        raise RuntimeError("reference package specdec not installed (baseline/_ref)")
+    Dec, Coin, Shim = make_models(S)
+    verify = Dec(rv)
     t0 = time.perf_counter()
-    O.decode_ar(rv, prompt, n_tokens)
-    ar_s = time.perf_counter() - t0
-    toks, _, cnt, wall = O.thread_async(cd, rv, prompt, n_tokens)
-    return {"amusd_tokens_per_s": len(toks) / wall, "ar_tokens_per_s": n_tokens / ar_s, "amusd_wall_s": wall,
-            "ar_wall_s": ar_s}
+    ar = S.decode_autoregressive(verify, prompt, S.DecodeConfig(max_new_tokens=n_tokens + 8, draft_window_k=k))
+    ar_wall = time.perf_counter() - t0
+    canon = list(prompt) + ar.tokens          # the coin's canonical path (SURVEY.md section 0.4)
+    draft = Coin(rd, canon, rho, 1234)
+    cfg = S.DecodeConfig(max_new_tokens=n_tokens, draft_window_k=k)
+    walls, toks, stats = [], 0, []
+    for i in range(warmup + steps):
+        ex = Shim()
+        res = S.decode_speculative_async(draft, verify, prompt, cfg, executor=ex)
+        if res.tokens != ar.tokens[:n_tokens]:
+            raise SystemExit("reference CPU AMUSD output differs from reference CPU AR")
+        if i >= warmup:
+            walls.append(ex.last_wall_s)
+            toks += len(res.tokens)
+            stats.append(res.stats)
+    return {"ar_tokens": ar.tokens[:n_tokens], "ar_tokens_per_s": len(ar.tokens) / (ar.stats.total_ms / 1000.0),
+            "ar_wall_s_incl_prefill": ar_wall, "amusd_tokens_per_s": toks / sum(walls), "amusd_wall_s": sum(walls),
+            "amusd_tokens": toks, "verify_steps": statistics.mean(s.verify_steps for s in stats),
+            "rollbacks": statistics.mean(s.rollbacks for s in stats), "specdec": str(S.__file__)}
 
 
 def reference_arm(args, rank: int, world: int):
-    """--impl reference: the CPU restatement of the path timed on the host cores."""
-    import numpy as np  # noqa: F401
+    """--impl reference: the reference's own CPU path, timed on the host cores.
+
+    The unmodified reference engines (baseline/_ref) drive fp32 numpy decoders of the
+    cfg3 shapes (oracle/ref_decoder.py) whose bf16-valued weights are generated on the HOST
+    by the same splitmix64 stream the GPU fill uses (oracle/ref_models.synthetic_weights):
+    no GPU and no libamusd on this arm.  A step = one AMUSD decode of a bounded sample of
+    new tokens (the fp32 8B forward costs ~0.7 s per token on the host)."""
     if rank != 0:
         return
     cores = os.cpu_count() or 1
     try:
-        import torch
-        if not torch.cuda.is_available():
-            raise RuntimeError("weights are generated on the GPU (synthetic bf16 init) then copied to the host")
-        import paper_2410_17375_b200 as P
-        from paper_2410_17375_b200 import _lib as L
-        from paper_2410_17375_b200.engines import canonical_path
-        TC = P.TransformerConfig
+        import numpy as np  # noqa: F401
+        from paper_2410_17375_b200.models import weight_names, weight_shape
+        from oracle.ref_models import synthetic_weights
         N, Plen = args.new_tokens, args.prompt_len
-        max_seq = Plen + N + 2 * L.KMAX + 32
-        if args.shapes == "tiny":
-            vcfg, dcfg = TC.tiny_verify(max_seq=max_seq), TC.tiny_draft(max_seq=max_seq)
-        else:
-            vcfg, dcfg = TC.llama_8b(max_seq=max_seq), TC.llama_1b(max_seq=max_seq)
-        vm = P.TransformerModel(vcfg, seed=0)
-        dm = P.TransformerModel(dcfg, seed=1)
+        vcfg, dcfg = _shapes(args, Plen + N + 64)
+        wv = synthetic_weights([(n, weight_shape(vcfg, n)) for n in weight_names(vcfg)], 0, bf16=True)
+        wd = synthetic_weights([(n, weight_shape(dcfg, n)) for n in weight_names(dcfg)], 1, bf16=True)
+        rv, rd = cpu_decoders(vcfg, dcfg, wv, wd)
         prompt = synthetic_prompt(Plen, vcfg.vocab_size)
-        canon = canonical_path(vm, prompt, N + L.KMAX).tolist()
-        rv, rd = cpu_models(vm, dm, vcfg, dcfg)
-        del vm, dm
-        torch.cuda.empty_cache()
-    except Exception as exc:  # pragma: no cover - only on a box without the GPU stack
+        sample = max(1, args.cpu_tokens)
+        r = reference_cpu_run(rv, rd, prompt, args.rho, sample, steps=args.steps, warmup=args.warmup, k=args.k)
+    except Exception as exc:  # pragma: no cover - reference not installed / host too small
         print(json.dumps({"impl": "reference", "unavailable": f"{type(exc).__name__}: {exc}"}))
         return
-    from oracle import specdec_oracle as O
-    from oracle.ref_decoder import CanonCoinDraft
-    cd = CanonCoinDraft(rd, canon, args.rho, 1234)
-    sample = max(1, args.cpu_tokens // 2)
-    for _ in range(args.warmup):
-        O.thread_async(cd, rv, prompt, 1)
-    walls, toks = [], 0
-    for _ in range(args.steps):
-        t, _, _, wall = O.thread_async(cd, rv, prompt, sample)
-        walls.append(wall)
-        toks += len(t)
-    v = toks / sum(walls)
+    v = r["amusd_tokens_per_s"]
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "tokens/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1000 * sum(walls) / args.steps, 2),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1000 * r["amusd_wall_s"] / args.steps, 2),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (random-init weights, seeded prompt)",
-            "config": {"workload": WORKLOAD, "rho": args.rho, "new_tokens_per_step": sample},
-            "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "cores": cores, "kind": "port",
-                             "sample": f"AMUSD two-thread executor (oracle restatement of engines.py:409-531) on "
-                                       f"numpy fp32 1B/8B-shaped decoders, {sample} new tokens per step"},
+            "config": {"workload": WORKLOAD, "rho": args.rho, "sync_k": args.k, "new_tokens_per_step": sample,
+                       "truncated": f"{sample} of {args.new_tokens} new tokens per step (bounded CPU sample)"},
+            "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "cores": cores, "kind": "reference",
+                             "sample": f"unmodified reference engines ({r['specdec']}): decode_speculative_async "
+                                       f"(ThreadExecutor + trace shim) on numpy fp32 1B/8B-shaped decoders through "
+                                       f"the MockModel hooks, {sample} new tokens per step, decode only",
+                             "ar_tokens_per_s": round(r["ar_tokens_per_s"], 4),
+                             "verify_steps": r["verify_steps"], "rollbacks": r["rollbacks"]},
             "e2e": {"value": round(v, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
+
+
+def cpu_leg(args, out):
+    """cpu_baseline (the reference's own engines on the host cores, same weights/prompt/rho)
+    and the CPU-vs-GPU parity of the bench shapes: first-step logits of both models and the
+    first AR tokens of the verify model (fp32 CPU over the same bf16 weights vs bf16 GPU)."""
+    import numpy as np
+    vm, dm = out["vm"], out["dm"]
+    rv, rd = cpu_decoders(out["vcfg"], out["dcfg"], vm.host_weights(), dm.host_weights())
+    prompt = out["prompt"]
+    par = {}
+    for key, m, r in (("verify", vm, rv), ("draft", dm, rd)):
+        gl = out["first_logits"][key]
+        cl = r.start(prompt).last_logits
+        par[f"{key}_logit_max_abs_over_std"] = round(float(np.abs(gl - cl).max() / cl.std()), 6)
+        par[f"{key}_argmax_equal"] = bool(int(np.argmax(gl)) == int(np.argmax(cl)))
+    s = reference_cpu_run(rv, rd, prompt, args.rho, args.cpu_tokens, k=args.k)
+    gpu = out["canon"][len(prompt):len(prompt) + args.cpu_tokens]
+    match = sum(int(a == b) for a, b in zip(s["ar_tokens"], gpu))
+    par.update({"tolerance": "logits |gpu-cpu|max/std(cpu) <= 3e-2 (bf16 weights+KV, fp32 accumulate)",
+                "ar_tokens_cpu": s["ar_tokens"], "ar_tokens_gpu": gpu,
+                "ar_tokens_match": f"{match}/{len(gpu)}"})
+    cpu = {"value": round(s["amusd_tokens_per_s"], 4), "unit": "tokens/s", "cores": os.cpu_count(), "kind": "reference",
+           "sample": f"{args.cpu_tokens} new tokens, unmodified reference engines (decode_speculative_async with "
+                     f"ThreadExecutor + trace shim) on numpy fp32 1B/8B-shaped decoders via the MockModel hooks, "
+                     f"same weights/prompt/rho, decode only",
+           "ar_tokens_per_s": round(s["ar_tokens_per_s"], 4)}
+    return cpu, par
 
 
 # -------------------------------------------------------------------- main
@@ -407,15 +454,9 @@ def main():
         if out is None:
             return
         res = out["results"]
-        cpu = None
+        cpu, parity = None, None
         if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.no_extras:
-            rv, rd = cpu_models(out["vm"], out["dm"], out["vcfg"], out["dcfg"])
-            s = cpu_sample(rv, rd, out["prompt"], out["canon"], args.rho, args.cpu_tokens)
-            cpu = {"value": round(s["amusd_tokens_per_s"], 4), "unit": "tokens/s", "cores": os.cpu_count(),
-                   "kind": "port",
-                   "sample": f"{args.cpu_tokens} new tokens, AMUSD two-thread executor + AR on numpy fp32 "
-                             f"1B/8B-shaped decoders (oracle/), same prompt/weights/rho",
-                   "ar_tokens_per_s": round(s["ar_tokens_per_s"], 4)}
+            cpu, parity = cpu_leg(args, out)
         if rank == 0:
             nan = {"tokens_per_s": float("nan"), "ms_per_step": float("nan"), "gpu_launches": 0}
             a, sy, ar = res.get("amusd", nan), res.get("sync", nan), res.get("ar", nan)
@@ -434,7 +475,7 @@ def main():
                 "ar": {k: round(v, 3) for k, v in ar.items()},
                 "speedup_vs_sync": round(a["tokens_per_s"] / sy["tokens_per_s"], 3),
                 "speedup_vs_ar": round(a["tokens_per_s"] / ar["tokens_per_s"], 3),
-                "roofline": out["roofline"], "cpu_baseline": cpu, "e2e": out["e2e"],
+                "roofline": out["roofline"], "cpu_baseline": cpu, "parity": parity, "e2e": out["e2e"],
                 "gpu_launches": int(a["gpu_launches"]), "clocks": out["clocks"],
             }
             print(json.dumps(line))

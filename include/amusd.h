@@ -102,6 +102,14 @@ size_t amusd_hash_state_bytes(int max_seq);
 int amusd_hash_create(amusd_model** out, uint64_t seed, int vocab, int eos_token, int exclude_eos,
                       double agreement_rho, int max_seq, void* state, size_t state_bytes);
 
+/* ScriptedModel (models.py:317-346): the prediction at 1-based absolute
+ * position p is script[(p-1) % script_len], or eos_token at eos_position
+ * (0 = none) -- pins eos-terminated run lengths (pkg/tests/test_engines.py:66-76).
+ * The script (host buffer) is copied into the caller's state buffer. */
+size_t amusd_scripted_state_bytes(int max_seq, int script_len);
+int amusd_scripted_create(amusd_model** out, const int32_t* script, int script_len, int vocab, int eos_token,
+                          int eos_position, int max_seq, void* state, size_t state_bytes, void* stream);
+
 int amusd_model_destroy(amusd_model* m);
 
 /* Forward implementation of a bf16 tensor-core-shaped transformer (perf A/B
@@ -111,6 +119,10 @@ int amusd_model_destroy(amusd_model* m);
  * Applies to launches enqueued afterwards (sessions capture it per engine). */
 enum { AMUSD_PATH_PERSISTENT = 0, AMUSD_PATH_KERNELS = 1, AMUSD_PATH_SIMT = 2 };
 int amusd_model_set_path(amusd_model* m, int path);
+/* Drop the caller's row-major layer weights from the model (the persistent path
+ * reads only its tile-contiguous copy): afterwards the caller may free them
+ * (8B: 16 GB) and only AMUSD_PATH_PERSISTENT remains selectable. */
+int amusd_model_release_row_major(amusd_model* m);
 /* Perf analysis only: run amusd_time_forward's persistent launches on `sms`
  * SMs (0 = all), e.g. the share a co-located session gives the model. */
 int amusd_model_set_grid(amusd_model* m, int sms);
@@ -178,6 +190,7 @@ typedef struct {
   int verify_steps, rollbacks, drafted, acks;
   int n_draft_events, n_verify_events;
   int draft_iters, verify_iters;  /* loop-body executions (launch accounting) */
+  int draft_cuts;                 /* draft forwards cut short by a rollback/completion (cumulative) */
 } amusd_run_info;
 int amusd_session_info(amusd_session* s, amusd_run_info* info, int32_t* V, int v_cap, void* stream);
 
@@ -215,8 +228,9 @@ int amusd_fill_uniform(void* dst, int dtype, size_t n, uint64_t seed, float scal
 int amusd_ipc_export(void* ptr, uint8_t handle[64], size_t* offset);
 int amusd_ipc_import(const uint8_t handle[64], size_t offset, void** ptr, void** base);
 int amusd_ipc_close(void* base);
-/* %globaltimer of this device (ns), for aligning the two GPUs' trace clocks. */
-int amusd_device_clock(int64_t* ns, void* stream);
+/* %globaltimer of this device (ns), for aligning the two GPUs' trace clocks;
+ * `scratch` is a caller-owned device buffer of >= 8 bytes. */
+int amusd_device_clock(int64_t* ns, void* scratch, void* stream);
 
 #ifdef __cplusplus
 }

@@ -121,6 +121,7 @@ class RefDecoder:
             a = (gg / (1.0 + np.exp(-gg))) * uu
             h = h + a @ w[p + "wdown"].T
         logits = self._normed_matmul(h, w["final_norm"], self.lm)
+        self.scratch = (newk, newv)   # the KV this forward produced (ref_models reuses it on advance)
         if commit:
             st.k, st.v = newk, newv
             st.tokens.extend(int(t) for t in toks)

@@ -36,6 +36,8 @@ def __getattr__(name):
     # device-facing modules import torch/libamusd lazily so that the pure host
     # pieces (errors, metrics, coordination) import without a GPU stack.
     import importlib
+    if name.startswith("_"):  # private submodules (_lib) resolve through the import system
+        raise AttributeError(name)
     if name in _LAZY:
         return importlib.import_module(f"{__name__}.{name}")
     for mod in _LAZY:
@@ -49,7 +51,7 @@ __all__ = [
     "ACTOR_DRAFT", "ACTOR_VERIFY", "AgreementDraft", "AgreementDraftModel", "ConfigError", "CudaAsyncExecutor",
     "CudaModel", "DecodeConfig", "DecodeResult", "DecodeStats", "DecodeTrace", "DeviceSession", "HashChainModel",
     "InvalidInputError", "InvalidRollbackError", "ModelState", "ProtocolViolationError", "RollbackRequest",
-    "SharedDecodeState", "SimulatorError", "SpecDecError", "TokenBuffer", "TraceEvent", "TransformerConfig",
+    "ScriptedModel", "SharedDecodeState", "SimulatorError", "SpecDecError", "TokenBuffer", "TraceEvent", "TransformerConfig",
     "TransformerModel", "busy_intervals", "canonical_path", "decode_autoregressive", "decode_speculative_async",
     "decode_speculative_sync", "find_mismatch", "finalize_tokens", "make_agreement_pair", "overlap_ms",
     "summarize", "trace_to_csv",

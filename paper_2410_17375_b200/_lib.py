@@ -50,7 +50,7 @@ class SessionDesc(C.Structure):
 class RunInfo(C.Structure):
     _fields_ = [(n, C.c_int) for n in ("p_v", "p_d", "complete", "error", "verify_steps", "rollbacks",
                                          "drafted", "acks", "n_draft_events", "n_verify_events",
-                                         "draft_iters", "verify_iters")]
+                                         "draft_iters", "verify_iters", "draft_cuts")]
 
 
 class TraceEvent(C.Structure):
@@ -67,9 +67,12 @@ SIGNATURES = [
     ("amusd_tf_create", _I, [_P(_VP), _P(TfConfig), _P(TfWeights), _VP, _SZ]),
     ("amusd_hash_state_bytes", _SZ, [_I]),
     ("amusd_hash_create", _I, [_P(_VP), C.c_uint64, _I, _I, _I, C.c_double, _I, _VP, _SZ]),
+    ("amusd_scripted_state_bytes", _SZ, [_I, _I]),
+    ("amusd_scripted_create", _I, [_P(_VP), _P(C.c_int32), _I, _I, _I, _I, _I, _VP, _SZ, _VP]),
     ("amusd_model_destroy", _I, [_VP]),
     ("amusd_model_set_path", _I, [_VP, _I]),
     ("amusd_model_set_grid", _I, [_VP, _I]),
+    ("amusd_model_release_row_major", _I, [_VP]),
     ("amusd_model_set_timeline", _I, [_VP, _VP, _SZ]),
     ("amusd_init_state", _I, [_VP, _P(C.c_int32), _I, _VP]),
     ("amusd_next_token", _I, [_VP, _P(C.c_int32), _VP]),
@@ -94,7 +97,7 @@ SIGNATURES = [
     ("amusd_ipc_export", _I, [_VP, _P(C.c_uint8), _P(_SZ)]),
     ("amusd_ipc_import", _I, [_P(C.c_uint8), _SZ, _P(_VP), _P(_VP)]),
     ("amusd_ipc_close", _I, [_VP]),
-    ("amusd_device_clock", _I, [_P(C.c_int64), _VP]),
+    ("amusd_device_clock", _I, [_P(C.c_int64), _VP, _VP]),
 ]
 
 _lib = None

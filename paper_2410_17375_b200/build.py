@@ -14,8 +14,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
-    "-shared",
 ]
+OBJ = PKG / "build"
 
 
 def sources():
@@ -33,11 +33,20 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not needs_build():
         return LIB
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [NVCC, *FLAGS, *map(str, sources()), "-o", str(tmp)]
+    # one nvcc per translation unit, in parallel (no cross-TU device code: no -rdc), then link
+    from concurrent.futures import ThreadPoolExecutor
+    OBJ.mkdir(exist_ok=True)
+    cmds = [[NVCC, *FLAGS, "-c", str(src), "-o", str(OBJ / (src.stem + ".o"))] for src in sources()]
     if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+        for c in cmds:
+            print(" ".join(c), file=sys.stderr)
+    with ThreadPoolExecutor(len(cmds)) as ex:
+        rcs = list(ex.map(lambda c: subprocess.run(c).returncode, cmds))
+    if any(rcs):
+        raise subprocess.CalledProcessError(max(rcs), "nvcc")
+    tmp = LIB.with_suffix(".so.tmp")
+    subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                    *[str(OBJ / (s.stem + ".o")) for s in sources()], "-o", str(tmp)], check=True)
     os.replace(tmp, LIB)
     return LIB
 

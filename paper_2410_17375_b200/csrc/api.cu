@@ -75,6 +75,9 @@ struct amusd_model {
   unsigned long long* chain = nullptr;
   bool agree = false, agree_always = false;
   unsigned long long agree_thr = 0;
+  // scripted model (models.py:317-346): device script table, 0 = none
+  int* script = nullptr;
+  int script_len = 0, eos_position = 0;
   // transformer
   amusd_tf_config cfg{};
   amusd_tf_weights w{};
@@ -123,6 +126,7 @@ struct amusd_model {
   size_t fw_ws_floats = 0, fw_cnt_ints = 0, fw_attn_cnt_ints = 0;  // cut cleanup extents
   int grid_override = 0;            // amusd_model_set_grid: SMs of amusd_time_forward launches (0 = all)
   int path = AMUSD_PATH_PERSISTENT;
+  bool row_major = true;  // row-major layer weights still valid (amusd_model_release_row_major)
   long long* fw_dbg = nullptr;  // optional per-item timeline (amusd_model_set_timeline)
   int fw_dbg_items = 0;
 };
@@ -142,16 +146,7 @@ static int fw_units() {
   if (v < 0) v = std::max(1, env_int("AMUSD_FW_UNITS", 16));
   return v;
 }
-static int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+static int num_sms() { return device_sms(); }
 // Deepest weight ring that fits `per_sm` CTAs on one SM (227 KB smem per SM).
 static int fw_max_stages(const amusd_tf_config& c, int per_sm) {
   const int group = c.n_heads / c.n_kv_heads;
@@ -268,13 +263,14 @@ static size_t tf_carve(const amusd_tf_config* c, void* base, amusd_model* m) {
   return align_up(cv.off, 256);
 }
 
-static size_t hash_carve(int max_seq, void* base, amusd_model* m) {
+static size_t hash_carve(int max_seq, void* base, amusd_model* m, int script_len = 0) {
   Carver cv(base);
   SeqHdr* seq = cv.take<SeqHdr>(1);
   int* tok = cv.take<int>(max_seq + 1);
   StepCtl* ctl = cv.take<StepCtl>(1);
   unsigned long long* chain = cv.take<unsigned long long>(max_seq + 2);
-  if (m) { m->seq = seq; m->tok = tok; m->api_ctl = ctl; m->chain = chain; }
+  int* script = script_len ? cv.take<int>(script_len) : nullptr;
+  if (m) { m->seq = seq; m->tok = tok; m->api_ctl = ctl; m->chain = chain; m->script = script; }
   return align_up(cv.off, 256);
 }
 
@@ -445,7 +441,7 @@ static int fw_forward(amusd_model* m, StepCtl* ctl, cudaStream_t st, bool want_l
   a.fine = env_int("AMUSD_FW_FINE", 0);  // per-tile deps measured slower: CTAs run their queues in order
   CUDA_TRY(fw::launch_forward(a, m->map_xa, m->map_attn, m->map_act, m->map_xb, m->fw_grid, m->fw_stages, st));
   if (a.ab_req)
-    CUDA_TRY(fw::launch_cut_cleanup(m->fw_sched, m->fw_ws, m->fw_ws_floats, m->fw_tile_cnt, m->fw_cnt_ints,
+    CUDA_TRY(fw::launch_cut_cleanup(m->fw_sched, ctl, m->fw_ws, m->fw_ws_floats, m->fw_tile_cnt, m->fw_cnt_ints,
                                     m->fw_attn_cnt, m->fw_attn_cnt_ints, m->fw_best, st));
   return AMUSD_OK;
 }
@@ -453,10 +449,12 @@ static int fw_forward(amusd_model* m, StepCtl* ctl, cudaStream_t st, bool want_l
 // Enqueue one forward of `m` driven by control block `ctl` (rows <= nr).
 static int model_forward(amusd_model* m, StepCtl* ctl, int nr, cudaStream_t st, bool pdl, bool want_logits) {
   if (m->kind == 1) {
-    CUDA_TRY(launch_hash_forward(ctl, m->chain, m->vocab, m->eos, m->exclude_eos, m->agree, m->agree_always, m->agree_thr, st));
+    CUDA_TRY(launch_hash_forward(ctl, m->chain, m->vocab, m->eos, m->exclude_eos, m->agree, m->agree_always,
+                                 m->agree_thr, m->script, m->script_len, m->eos_position, st));
     return AMUSD_OK;
   }
   if (use_fw(m)) return fw_forward(m, ctl, st, want_logits);
+  if (!m->row_major) return fail(AMUSD_ERR_UNSUPPORTED, "row-major weights released: persistent path only");
   if (use_tc(m, nr)) {
     if (int r = tc_kernel(m, ctl, 0, 7, st, pdl)) return r;
     for (int l = 0; l < m->cfg.n_layers; ++l)
@@ -604,6 +602,43 @@ int amusd_hash_create(amusd_model** out, uint64_t seed, int vocab, int eos, int 
   return AMUSD_OK;
 }
 
+size_t amusd_scripted_state_bytes(int max_seq, int script_len) {
+  return hash_carve(max_seq, nullptr, nullptr, std::max(script_len, 1));
+}
+
+int amusd_scripted_create(amusd_model** out, const int32_t* script, int script_len, int vocab, int eos,
+                          int eos_position, int max_seq, void* state, size_t state_bytes, void* stream) {
+  if (!out || !state || !script) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  if (vocab < 2) return fail(AMUSD_ERR_INVALID_INPUT, "vocab_size must be >= 2");  // models.py:96
+  if (!(0 <= eos && eos < vocab)) return fail(AMUSD_ERR_INVALID_INPUT, "eos_token out of range");
+  if (script_len < 1) return fail(AMUSD_ERR_INVALID_INPUT, "script must contain at least one token");  // models.py:333
+  for (int i = 0; i < script_len; ++i)
+    if (script[i] < 0 || script[i] >= vocab)
+      return fail(AMUSD_ERR_INVALID_INPUT, "token " + std::to_string(script[i]) + " out of vocabulary range [0, " +
+                                               std::to_string(vocab) + ")");
+  if (eos_position < 0) return fail(AMUSD_ERR_INVALID_INPUT, "eos_position must be >= 1");  // models.py:336 (0 = none)
+  if (max_seq < 2) return fail(AMUSD_ERR_INVALID_INPUT, "max_seq must be >= 2");
+  if (state_bytes < amusd_scripted_state_bytes(max_seq, script_len))
+    return fail(AMUSD_ERR_INVALID_INPUT, "state buffer too small");
+  amusd_model* m = new amusd_model();
+  m->kind = 1;
+  m->vocab = vocab;
+  m->eos = eos;
+  m->max_seq = max_seq;
+  m->script_len = script_len;
+  m->eos_position = eos_position;
+  hash_carve(max_seq, state, m, script_len);
+  cudaError_t e = cudaMemcpyAsync(m->script, script, sizeof(int) * script_len, cudaMemcpyHostToDevice,
+                                  (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    delete m;
+    return fail(AMUSD_ERR_CUDA, std::string("script upload: ") + cudaGetErrorString(e));
+  }
+  *out = m;
+  return AMUSD_OK;
+}
+
 int amusd_model_destroy(amusd_model* m) {
   delete m;
   return AMUSD_OK;
@@ -621,9 +656,23 @@ int amusd_model_set_path(amusd_model* m, int path) {
   if (path < AMUSD_PATH_PERSISTENT || path > AMUSD_PATH_SIMT) return fail(AMUSD_ERR_INVALID_INPUT, "unknown path");
   if (path != AMUSD_PATH_SIMT && m->kind == 0 && !m->tc)
     return fail(AMUSD_ERR_UNSUPPORTED, "tensor-core paths need a bf16 model with 128-aligned shapes");
-  if (m->kind == 0 && m->cfg.dtype == AMUSD_BF16 && path == AMUSD_PATH_SIMT && !m->w.wgate[0])
-    return fail(AMUSD_ERR_UNSUPPORTED, "SIMT path needs row-major weights");
+  if (m->kind == 0 && path != AMUSD_PATH_PERSISTENT && !m->row_major)
+    return fail(AMUSD_ERR_UNSUPPORTED, "the row-major weights were released: only the persistent path remains");
   m->path = path;
+  return AMUSD_OK;
+}
+
+int amusd_model_release_row_major(amusd_model* m) {
+  if (!m) return fail(AMUSD_ERR_INVALID_INPUT, "null model");
+  if (m->kind != 0 || !m->tc || !m->fw_ready)
+    return fail(AMUSD_ERR_UNSUPPORTED, "only a tensor-core model on the persistent path can drop its row-major weights");
+  if (m->path != AMUSD_PATH_PERSISTENT)
+    return fail(AMUSD_ERR_UNSUPPORTED, "row-major weights are in use by the selected forward path");
+  CUDA_TRY(cudaDeviceSynchronize());  // no launch in flight reads them
+  for (int l = 0; l < m->cfg.n_layers; ++l)
+    m->w.wqkv[l] = m->w.wo[l] = m->w.wgate[l] = m->w.wup[l] = m->w.wdown[l] = nullptr;
+  if (m->w.lm_head != m->w.embed) m->w.lm_head = nullptr;
+  m->row_major = false;
   return AMUSD_OK;
 }
 
@@ -909,6 +958,10 @@ int amusd_session_create(amusd_session** out, amusd_model* draft, amusd_model* v
                          void* mem, size_t mem_bytes, void* mb_local, void* mb_peer) {
   if (!out || !d || !mem || !mb_local) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
   if (!draft && !verify) return fail(AMUSD_ERR_INVALID_INPUT, "session needs a draft or a verify model");
+  // a device model holds ONE sequence (KV cache, schedule counters, split-K workspace):
+  // the same handle as both draft and verify would run two forwards over the same state
+  if (draft == verify)
+    return fail(AMUSD_ERR_INVALID_INPUT, "draft and verify must be distinct device models (one sequence per model)");
   if (d->prompt_len < 1) return fail(AMUSD_ERR_INVALID_INPUT, "prompt_length must be >= 1");
   if (d->max_new_tokens < 1) return fail(AMUSD_ERR_INVALID_INPUT, "max_new_tokens must be >= 1");
   if (d->draft_window_k < 1 || d->draft_window_k > KMAX - 1)
@@ -988,9 +1041,6 @@ static int capture_body(amusd_session* s, int engine, int actor, cudaGraph_t bod
   // Co-located AMUSD: early-launched (PDL) verify CTAs would hold the second
   // SM slot and starve the draft stream -- measured 146 vs 221 tok/s on B200.
   const bool pdl = s->use_pdl && engine != AMUSD_ENGINE_ASYNC;
-  // Persistent-forward launch shape: co-located AMUSD runs the draft and the
-  // verify forward at the same time, so each gets a ring that lets two CTAs
-  // share an SM; every other engine owns the GPU (deepest ring, 1 CTA/SM).
   const bool colo = engine == AMUSD_ENGINE_ASYNC;
   // Co-located AMUSD: the draft and the verify forward run at the same time on DISJOINT SM
   // sets (each persistent CTA fills an SM; grids summing to <= #SMs can always co-run, and
@@ -1122,6 +1172,12 @@ int amusd_session_info(amusd_session* s, amusd_run_info* info, int32_t* V, int v
   info->n_verify_events = counts[1];
   info->draft_iters = h.db.iters;
   info->verify_iters = h.vb.iters;
+  info->draft_cuts = 0;
+  if (s->draft && s->draft->kind == 0 && s->draft->fw_sched) {
+    CUDA_TRY(cudaMemcpyAsync(&info->draft_cuts, fw::cut_counter(s->draft->fw_sched), sizeof(int),
+                             cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+  }
   if (V && v_cap > 0) {
     const int nv = std::min(v_cap, std::max(0, h.vb.p_v - s->d.prompt_len));
     if (nv) CUDA_TRY(cudaMemcpyAsync(V, mb_V(s->mb_local, s->cap), sizeof(int) * nv, cudaMemcpyDeviceToHost, st));
@@ -1185,6 +1241,8 @@ int amusd_time_forward(amusd_model* m, int rows, int which, int layer, int iters
 int amusd_session_kernels_per_step(amusd_session* s, int engine, int* draft_step, int* verify_step) {
   if (!s || !draft_step || !verify_step) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
   *draft_step = s->draft ? model_kernels_per_forward(s->draft, 2) + 2 : 0;
+  // the AMUSD draft's persistent forward is followed by the cut cleanup (a no-op launch when not cut)
+  if (engine == AMUSD_ENGINE_ASYNC && s->draft && use_fw(s->draft) && env_int("AMUSD_FW_CUT", 1)) *draft_step += 1;
   *verify_step = s->verify ? model_kernels_per_forward(s->verify, KMAX) + 2 : 0;
   if (engine == AMUSD_ENGINE_SYNC) *verify_step += 1;
   return AMUSD_OK;
@@ -1255,14 +1313,13 @@ int amusd_ipc_close(void* base) {
 
 __global__ void k_device_clock(long long* out) { *out = globaltimer(); }
 
-extern "C" int amusd_device_clock(int64_t* ns, void* stream) {
-  if (!ns) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
-  long long* d = nullptr;
-  CUDA_TRY(cudaMallocAsync((void**)&d, sizeof(long long), (cudaStream_t)stream));
+extern "C" int amusd_device_clock(int64_t* ns, void* scratch, void* stream) {
+  if (!ns || !scratch) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  long long* d = (long long*)scratch;  // caller-owned 8-byte device buffer (the library never allocates)
   k_device_clock<<<1, 1, 0, (cudaStream_t)stream>>>(d);
+  CUDA_TRY(cudaGetLastError());
   long long v = 0;
   CUDA_TRY(cudaMemcpyAsync(&v, d, sizeof(v), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
-  CUDA_TRY(cudaFreeAsync(d, (cudaStream_t)stream));
   CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
   *ns = v;
   return AMUSD_OK;

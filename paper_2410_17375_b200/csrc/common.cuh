@@ -8,6 +8,40 @@
 
 namespace amusd {
 
+// ---------------------------------------------------------- host helpers
+// Per-DEVICE host caches: one process may drive models on several GPUs (split pair),
+// so nothing device-specific is cached process-wide.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev >= 0 && dev < kMaxDevices ? dev : 0;
+}
+// SM count of the current device.
+inline int device_sms() {
+  static int n[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!n[dev]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    n[dev] = v;
+  }
+  return n[dev];
+}
+// Dynamic shared-memory opt-in of one kernel, applied once per device (largest size seen).
+struct SmemOptIn {
+  int bytes[kMaxDevices] = {};
+  template <class K>
+  cudaError_t ensure(K kern, int want) {
+    const int dev = current_device();
+    if (want <= bytes[dev]) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, want);
+    if (e == cudaSuccess) bytes[dev] = want;
+    return e;
+  }
+};
+
+
 // ---- memory ordering for the mailbox (single writer per field) -------------
 // Writers store payload, then st.release the counter/epoch; readers
 // ld.acquire the counter, then read payload.  .sys scope so the same code is

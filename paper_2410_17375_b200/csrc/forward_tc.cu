@@ -1120,7 +1120,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
         tc_fence_before();
         mbar_arrive(smem_u32(&tempty[b]));
         ++seg;
-        if (a.dbg && tid == 0 && v[0] != 12345.f) dbg_mark(a, phase_first(a, L, p) + j, 6, globaltimer());  // TEMP tmem read
         const int epi = g.epi, nchunks = g.nchunks;
         // RMSNorm scale of the phase's input rows (once per phase per CTA).  Only the merging
         // item scales (the scale is linear and applies to the exact sum): contributors skip
@@ -1183,7 +1182,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
           // with a fire-and-forget release and move on -- no round trip in their epilogue.
           final = cj == nchunks - 1;
           if (!final) {
-            if (a.dbg && tid == 0) dbg_mark(a, phase_first(a, L, p) + j, 2, globaltimer());  // TEMP reds+bar done
             if (tid == 0) {
               if (a.debug & 32) red_add_relaxed(a.tile_cnt + g.cnt_off + t * kPad, 1);  // timing experiment only
               else red_add_release(a.tile_cnt + g.cnt_off + t * kPad, 1);
@@ -1322,25 +1320,43 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
 }
 
-__global__ void __launch_bounds__(1024) k_cut_cleanup(int* flag, float* ws, size_t ws_floats, int* tile_cnt,
-                                                      size_t cnt_ints, int* attn_cnt, size_t attn_cnt_ints,
-                                                      unsigned long long* best) {
+// Re-arm the split-K state a draft cut left behind (a no-op when the forward was not cut).
+// Only the live rows of the int64 accumulators were ever added (k_forward adds rows < rows), so
+// only those are cleared; the work is spread over kCleanCtas CTAs and the last one out clears
+// the flag and counts the cut (sched layout: [2*kPad] epoch, +1 cut flag, +2 cuts, +3 exit count).
+constexpr int kCleanCtas = 16;
+__global__ void __launch_bounds__(512) k_cut_cleanup(int* sched, const StepCtl* ctl, unsigned long long* ws,
+                                                     size_t ws_blocks, int* tile_cnt, size_t cnt_ints, int* attn_cnt,
+                                                     size_t attn_cnt_ints, unsigned long long* best) {
+  int* flag = sched + 2 * kPad + 1;
   if (ld_volatile(flag) == 0) return;  // not cut: nothing to re-arm
-  uint4* w = (uint4*)ws;               // (16-byte aligned carve; ws_floats is even)
-  const size_t nw = ws_floats / 4;
-  for (size_t i = threadIdx.x; i < nw; i += blockDim.x) w[i] = make_uint4(0, 0, 0, 0);
-  for (size_t i = nw * 4 + threadIdx.x; i < ws_floats; i += blockDim.x) ws[i] = 0.f;
-  for (size_t i = threadIdx.x; i < cnt_ints; i += blockDim.x) tile_cnt[i] = 0;
-  for (size_t i = threadIdx.x; i < attn_cnt_ints; i += blockDim.x) attn_cnt[i] = 0;
-  if (threadIdx.x < KMAX) best[threadIdx.x] = 0ull;
+  const int rows = max(1, min(KMAX, ctl->rows));
+  const size_t per_block = (size_t)rows * BM;  // live rows of one [16][128] tile block
+  const size_t n = ws_blocks * per_block;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    ws[(i / per_block) * (BN * BM) + i % per_block] = 0ull;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < cnt_ints; i += (size_t)gridDim.x * blockDim.x)
+    tile_cnt[i] = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < attn_cnt_ints; i += (size_t)gridDim.x * blockDim.x)
+    attn_cnt[i] = 0;
+  if (blockIdx.x == 0 && threadIdx.x < KMAX) best[threadIdx.x] = 0ull;
   __syncthreads();
-  if (threadIdx.x == 0) *flag = 0;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(sched + 2 * kPad + 3, 1) == (int)gridDim.x - 1) {
+      sched[2 * kPad + 3] = 0;
+      sched[2 * kPad + 2] += 1;  // cuts so far (amusd_run_info.draft_cuts)
+      *flag = 0;
+    }
+  }
 }
 
-cudaError_t launch_cut_cleanup(int* sched, float* ws, size_t ws_floats, int* tile_cnt, size_t cnt_ints,
-                               int* attn_cnt, size_t attn_cnt_ints, unsigned long long* best, cudaStream_t st) {
-  k_cut_cleanup<<<1, 1024, 0, st>>>(sched + 2 * kPad + 1, ws, ws_floats, tile_cnt, cnt_ints, attn_cnt, attn_cnt_ints,
-                                    best);
+cudaError_t launch_cut_cleanup(int* sched, const StepCtl* ctl, float* ws, size_t ws_floats, int* tile_cnt,
+                               size_t cnt_ints, int* attn_cnt, size_t attn_cnt_ints, unsigned long long* best,
+                               cudaStream_t st) {
+  static_assert(BN == KMAX, "accumulator blocks are [KMAX rows][BM]");
+  k_cut_cleanup<<<kCleanCtas, 512, 0, st>>>(sched, ctl, (unsigned long long*)ws, ws_floats / 2 / (BN * BM), tile_cnt,
+                                            cnt_ints, attn_cnt, attn_cnt_ints, best);
   return cudaGetLastError();
 }
 
@@ -1349,15 +1365,7 @@ int attn_items_max(int KV, int S) { return KV * KMAX * attn_splits(S); }
 int attn_splits(int S) { return (S + kAttnChunk - 1) / kAttnChunk; }
 int max_positions() { return kMaxMerge * kAttnChunk; }
 
-static int num_sms_host() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
-  }
-  return n;
-}
+static int num_sms_host() { return device_sms(); }
 
 // Units per item: the largest divisor of kb that is <= target and a whole number of ring
 // stages (kb is even for every supported shape: tc_shapes_ok).
@@ -1468,12 +1476,8 @@ template <int HD, int G, int MINB>
 static cudaError_t launch_m(const FwArgs& a, const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& m2,
                             const CUtensorMap& m3, int grid, int stages, cudaStream_t st) {
   const int smem = forward_smem_bytes(stages, HD, G);
-  static int attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_forward<HD, G, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
+  static SmemOptIn opt;  // per device (one process may hold models on two GPUs)
+  if (cudaError_t e = opt.ensure(k_forward<HD, G, MINB>, smem)) return e;
   FwArgs b = a;
   b.stages = stages;
   k_forward<HD, G, MINB><<<grid, kThreads, smem, st>>>(m0, m1, m2, m3, b);

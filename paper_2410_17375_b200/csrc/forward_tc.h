@@ -123,8 +123,11 @@ cudaError_t launch_forward(const FwArgs& a, const CUtensorMap& m_xa, const CUten
                            const CUtensorMap& m_act, const CUtensorMap& m_xb, int grid, int stages, cudaStream_t st);
 // After a forward launched with ab_req: if it was cut (flag in the schedule), zero the split-K
 // accumulators / counters, attention counters and argmax keys (one CTA; a no-op otherwise).
-cudaError_t launch_cut_cleanup(int* sched, float* ws, size_t ws_floats, int* tile_cnt, size_t cnt_ints,
-                               int* attn_cnt, size_t attn_cnt_ints, unsigned long long* best, cudaStream_t st);
+cudaError_t launch_cut_cleanup(int* sched, const StepCtl* ctl, float* ws, size_t ws_floats, int* tile_cnt,
+                               size_t cnt_ints, int* attn_cnt, size_t attn_cnt_ints, unsigned long long* best,
+                               cudaStream_t st);
+// Draft cuts counted by the cleanup (sched line 2, int 2).
+inline int* cut_counter(int* sched) { return sched + 2 * kCounterInts + 2; }
 // schedule counters: grab, exit, epoch (+ cut flag), then one per phase (kCounterInts each)
 inline size_t sched_ints(int L) { return (size_t)(3 + num_phases(L)) * kCounterInts; }
 int forward_smem_bytes(int stages, int hd, int group);

@@ -441,15 +441,8 @@ bool make_map(CUtensorMap* m, const void* ptr, int rows, int cols, int box_rows)
   return r == CUDA_SUCCESS;
 }
 
-static int g_num_sms = 0;
-
 int tc_grid(int ntiles, int kb) {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
+  const int g_num_sms = device_sms();
   static int cap = -1;
   if (cap < 0) {  // AMUSD_TC_GRID: leave SMs to a co-located draft (scheduling knob)
     const char* e = getenv("AMUSD_TC_GRID");
@@ -461,11 +454,8 @@ int tc_grid(int ntiles, int kb) {
 }
 
 cudaError_t launch_gemm_tc(const CUtensorMap& mx, const TcArgs& a, cudaStream_t st, bool pdl) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes());
-    attr = true;
-  }
+  static SmemOptIn opt;  // per device
+  if (cudaError_t e = opt.ensure(k_gemm_tc, smem_bytes())) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tc_grid(a.ntiles, a.kb));
   cfg.blockDim = dim3(kThreads);

@@ -438,11 +438,18 @@ __global__ void k_session_reset(ProtoArgs a, const int* prompt, unsigned long lo
 // index pos0+j (h[pos0+j+1] = splitmix64(h[pos0+j] ^ tok)) and predicts the
 // next token from it (models.py:221-235, 256-268).
 __global__ void k_hash_forward(StepCtl* c, unsigned long long* h, int vocab, int eos, int exclude_eos, int agree,
-                               int always, unsigned long long thr) {
+                               int always, unsigned long long thr, const int* script, int script_len, int eos_pos) {
   pdl_wait();
   if (threadIdx.x != 0 || !c->active) return;
   for (int j = 0; j < c->rows; ++j) {
     const int p = c->pos0 + j;
+    if (script) {
+      // ScriptedModel._predict (models.py:340-344): the token at 1-based absolute position
+      // prefix_length + 1, where prefix_length = p + 1 after consuming row j
+      const int pos1 = p + 2;
+      c->preds[j] = pos1 == eos_pos ? eos : script[(pos1 - 1) % script_len];
+      continue;
+    }
     const unsigned long long hp = mix64(h[p] ^ (unsigned long long)(unsigned)c->tok[j]);
     h[p + 1] = hp;
     const int base = chain_draw(hp, vocab, eos, exclude_eos);
@@ -480,8 +487,9 @@ cudaError_t launch_session_reset(const ProtoArgs& a, const int* prompt_dev, unsi
 }
 
 cudaError_t launch_hash_forward(StepCtl* c, unsigned long long* h, int vocab, int eos, int excl, int agree, int always,
-                                unsigned long long thr, cudaStream_t st) {
-  k_hash_forward<<<1, 32, 0, st>>>(c, h, vocab, eos, excl, agree, always, thr);
+                                unsigned long long thr, const int* script, int script_len, int eos_pos,
+                                cudaStream_t st) {
+  k_hash_forward<<<1, 32, 0, st>>>(c, h, vocab, eos, excl, agree, always, thr, script, script_len, eos_pos);
   return cudaGetLastError();
 }
 cudaError_t launch_hash_seed(unsigned long long* h, unsigned long long seed, cudaStream_t st) {

@@ -15,7 +15,8 @@ cudaError_t proto_launch(int which, const ProtoArgs& a, cudaStream_t st, int arg
 cudaError_t launch_session_reset(const ProtoArgs& a, const int* prompt_dev, unsigned long long coin_seed,
                                  cudaStream_t st);
 cudaError_t launch_hash_forward(StepCtl* c, unsigned long long* h, int vocab, int eos, int excl, int agree, int always,
-                                unsigned long long thr, cudaStream_t st);
+                                unsigned long long thr, const int* script, int script_len, int eos_pos,
+                                cudaStream_t st);
 cudaError_t launch_hash_seed(unsigned long long* h, unsigned long long seed, cudaStream_t st);
 
 }  // namespace amusd

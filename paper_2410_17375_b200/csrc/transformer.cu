@@ -451,11 +451,8 @@ static cudaError_t gemv_launch(const GemvArgs& a, cudaStream_t st, bool pdl) {
   const int grid = (a.N + rows_per_cta - 1) / rows_per_cta;
   const size_t smem = (size_t)NR * a.kc * sizeof(float);
   auto kern = k_gemv<NR, WT, EPI, RPW>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    attr_set = true;
-  }
+  static SmemOptIn opt;  // per device
+  if (cudaError_t e = opt.ensure(kern, 96 * 1024)) return e;
   return launch_pdl(kern, dim3(grid), dim3(kGemvThreads), smem, st, pdl, a);
 }
 

@@ -17,6 +17,8 @@ passes ``DecodeTrace.validate``.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
+from collections import OrderedDict
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -129,10 +131,14 @@ class DeviceSession:
                  canon: torch.Tensor | None = None, trace_cap: int | None = None, jitter_ns: int = 0,
                  jitter_seed: int = 0, mb_peer: int | None = None, mb_local: torch.Tensor | None = None):
         self.lib = L.load()
-        self.draft = draft
-        self.verify = verify
+        # weak: a cached session must not keep its models (GBs of HBM) alive (see _session)
+        self._draft = weakref.ref(draft) if draft is not None else None
+        self._verify = weakref.ref(verify) if verify is not None else None
         dm = _model_of(draft) if draft is not None else None
         vm = _model_of(verify) if verify is not None else None
+        if dm is not None and dm is vm:
+            raise InvalidInputError("draft and verify must be distinct device models: a CudaModel holds one "
+                                    "live sequence (KV cache and forward workspace)")
         self.device = (vm or dm).device
         self.config = config
         self.prompt_len = prompt_len
@@ -162,6 +168,14 @@ class DeviceSession:
         settle(self.device)
         self._trace_buf = (L.TraceEvent * cap)()
         self._v_buf = (C.c_int32 * (self.mb_cap + 1))()
+
+    @property
+    def draft(self):
+        return self._draft() if self._draft is not None else None
+
+    @property
+    def verify(self):
+        return self._verify() if self._verify is not None else None
 
     @staticmethod
     def mailbox_bytes(prompt_len: int, config: DecodeConfig) -> int:
@@ -238,14 +252,33 @@ class DeviceSession:
             pass
 
 
-_SESSIONS: dict = {}
+# Cached sessions / canonical paths, keyed by model identity.  Entries hold their models
+# only weakly and are evicted when a model (or AgreementDraft wrapper) is collected; the
+# session cache is also LRU-bounded, so a caller looping over models never accumulates HBM.
+_SESSIONS: "OrderedDict" = OrderedDict()
 _CANON: dict = {}
+_TRACKED: set = set()
+MAX_SESSIONS = 16
 
 
 def clear_sessions() -> None:
-    """Drop cached device sessions and canonical paths (and the models they pin)."""
+    """Drop cached device sessions and canonical paths."""
     _SESSIONS.clear()
     _CANON.clear()
+
+
+def _evict(key: int) -> None:
+    _TRACKED.discard(key)
+    for k in [k for k in _SESSIONS if key in (k[0], k[1])]:
+        del _SESSIONS[k]
+    for k in [k for k in _CANON if k[0] == key]:
+        del _CANON[k]
+
+
+def _track(obj) -> None:
+    if obj is not None and id(obj) not in _TRACKED:
+        _TRACKED.add(id(obj))
+        weakref.finalize(obj, _evict, id(obj))
 
 
 def _session(draft, verify, prompt_len, config, **kw) -> DeviceSession:
@@ -255,8 +288,14 @@ def _session(draft, verify, prompt_len, config, **kw) -> DeviceSession:
            None if canon is None else canon.data_ptr(), getattr(draft, "agreement_rho", None))
     s = _SESSIONS.get(key)
     if s is None:
+        _track(draft)
+        _track(verify)
         s = DeviceSession(draft, verify, prompt_len, config, **kw)
         _SESSIONS[key] = s
+        while len(_SESSIONS) > MAX_SESSIONS:
+            _SESSIONS.popitem(last=False)
+    else:
+        _SESSIONS.move_to_end(key)
     return s
 
 
@@ -268,6 +307,7 @@ def canonical_path(verify, prompt: Sequence[int], n: int) -> torch.Tensor:
     vm = _model_of(verify)
     key = (id(vm), tuple(prompt), n)
     if key not in _CANON:
+        _track(vm)
         cfg = DecodeConfig(max_new_tokens=n)
         out = _session(None, verify, len(prompt), cfg).run(L.ENGINE_AR, prompt)
         toks = list(prompt) + out.verified

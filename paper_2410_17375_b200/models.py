@@ -35,7 +35,7 @@ from . import _lib as L
 from .errors import InvalidInputError
 
 __all__ = [
-    "ModelState", "CudaModel", "HashChainModel", "AgreementDraftModel", "make_agreement_pair",
+    "ModelState", "CudaModel", "HashChainModel", "AgreementDraftModel", "ScriptedModel", "make_agreement_pair",
     "TransformerConfig", "TransformerModel", "AgreementDraft", "device_stream",
 ]
 
@@ -200,6 +200,34 @@ class AgreementDraftModel(HashChainModel):
         self.agreement_rho = agreement_rho
 
 
+class ScriptedModel(CudaModel):
+    """Prediction depends only on the absolute position (models.py:317-346), on the GPU:
+    ``script[i]`` is the token at 1-based absolute position ``i + 1`` (cycling), and
+    ``eos_position`` forces ``eos_token`` there -- the reference's eos edge-case model."""
+
+    def __init__(self, script: Sequence[int], vocab_size: int, eos_token: int, eos_position: int | None = None,
+                 max_seq: int = 4096, device=None):
+        super().__init__(vocab_size, eos_token, device)
+        if len(script) == 0:
+            raise InvalidInputError("script must contain at least one token")
+        self._validate_tokens(script)
+        if eos_position is not None and eos_position < 1:
+            raise InvalidInputError(f"eos_position must be >= 1, got {eos_position}")
+        self.script = list(script)
+        self.eos_position = eos_position
+        nbytes = self._lib.amusd_scripted_state_bytes(max_seq, len(script))
+        self._state = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
+        settle(self.device)
+        with torch.cuda.device(self.device):
+            L.check(self._lib.amusd_scripted_create(C.byref(self._h), L.int_array(script), len(script), vocab_size,
+                                                    eos_token, eos_position or 0, max_seq,
+                                                    C.c_void_p(self._state.data_ptr()), nbytes,
+                                                    device_stream(self.device)))
+
+    def kernels_per_forward(self) -> int:
+        return 1
+
+
 def make_agreement_pair(seed: int, rho: float, vocab_size: int, eos_token: int, exclude_eos: bool = False,
                         max_seq: int = 4096, device=None):
     """(draft, verify) with per-position agreement rho (models.py:349-365)."""
@@ -310,7 +338,7 @@ class TransformerModel(CudaModel):
     """Llama-style decoder whose forwards are libamusd CUDA kernels."""
 
     def __init__(self, config: TransformerConfig, weights: dict | None = None, seed: int = 0,
-                 device=None, init_std: float = 0.02):
+                 device=None, init_std: float = 0.02, keep_row_major: bool = True):
         super().__init__(config.vocab_size, config.eos_token, device)
         if config.dtype not in ("bf16", "fp32"):
             raise InvalidInputError(f"dtype must be 'bf16' or 'fp32', got {config.dtype!r}")
@@ -319,8 +347,10 @@ class TransformerModel(CudaModel):
         self.config = config
         self.seed = seed
         tdt = torch.bfloat16 if config.dtype == "bf16" else torch.float32
+        self._synth = None
         if weights is None:
             weights = self._synthetic(tdt, seed, init_std)
+            self._synth = (tdt, seed, init_std)
         else:
             weights = {k: v.to(device=self.device, dtype=tdt).contiguous() for k, v in weights.items()}
         for n in weight_names(config):
@@ -352,23 +382,37 @@ class TransformerModel(CudaModel):
         L.check(self._lib.amusd_tf_create(C.byref(self._h), C.byref(cfg), C.byref(w),
                                           C.c_void_p(self._state.data_ptr()), nbytes))
         settle(self.device)
+        self.row_major = True
+        if not keep_row_major:
+            self.release_row_major()
+
+    def release_row_major(self) -> None:
+        """Free the row-major layer weights (the persistent forward streams only its
+        tile-contiguous copy): halves the model's HBM (8B: 16 GB).  Only the persistent
+        path stays selectable; ``host_weights`` regenerates synthetic weights by seed."""
+        with torch.cuda.device(self.device):
+            L.check(self._lib.amusd_model_release_row_major(self._h))
+        keep = {"embed", "final_norm"} | {n for n in self.weights if n.endswith("norm")}
+        self._dropped = [n for n in self.weights if n not in keep]
+        for n in self._dropped:
+            del self.weights[n]
+        self.row_major = False
+        torch.cuda.empty_cache()
+    def _synthetic_one(self, i: int, n: str, tdt, seed: int, std: float):
+        t = torch.empty(weight_shape(self.config, n), dtype=tdt, device=self.device)
+        if n.endswith("norm"):
+            t.fill_(1.0)
+        else:
+            sub = (seed * 0x9E3779B97F4A7C15 + (i + 1) * 0xD1B54A32D192ED03) & ((1 << 64) - 1)
+            dt = L.BF16 if tdt == torch.bfloat16 else L.F32
+            with torch.cuda.device(self.device):
+                L.check(self._lib.amusd_fill_uniform(C.c_void_p(t.data_ptr()), dt, t.numel(), sub,
+                                                     std * math.sqrt(3.0), device_stream(self.device)))
+        return t
 
     def _synthetic(self, tdt, seed: int, std: float) -> dict:
         """Deterministic random init on the GPU: uniform with the given std, norms = 1."""
-        out = {}
-        scale = std * math.sqrt(3.0)
-        dt = L.BF16 if tdt == torch.bfloat16 else L.F32
-        for i, n in enumerate(weight_names(self.config)):
-            t = torch.empty(weight_shape(self.config, n), dtype=tdt, device=self.device)
-            if n.endswith("norm"):
-                t.fill_(1.0)
-            else:
-                sub = (seed * 0x9E3779B97F4A7C15 + (i + 1) * 0xD1B54A32D192ED03) & ((1 << 64) - 1)
-                with torch.cuda.device(self.device):
-                    L.check(self._lib.amusd_fill_uniform(C.c_void_p(t.data_ptr()), dt, t.numel(), sub, scale,
-                                                         device_stream(self.device)))
-            out[n] = t
-        return out
+        return {n: self._synthetic_one(i, n, tdt, seed, std) for i, n in enumerate(weight_names(self.config))}
 
     PATHS = {"persistent": L.PATH_PERSISTENT, "kernels": L.PATH_KERNELS, "simt": L.PATH_SIMT}
 
@@ -397,8 +441,17 @@ class TransformerModel(CudaModel):
         return out
 
     def host_weights(self) -> dict:
-        """fp32 numpy copies of every weight (for the CPU oracle / baseline)."""
-        return {k: v.float().cpu().numpy() for k, v in self.weights.items()}
+        """fp32 numpy copies of every weight (for the CPU oracle / baseline).  Released
+        synthetic weights are regenerated one at a time by the same device fill."""
+        out = {}
+        for i, n in enumerate(weight_names(self.config)):
+            if n in self.weights:
+                out[n] = self.weights[n].float().cpu().numpy()
+            elif self._synth is not None:
+                out[n] = self._synthetic_one(i, n, *self._synth).float().cpu().numpy()
+            else:
+                raise InvalidInputError(f"weight {n} was released (keep_row_major=False) and is not synthetic")
+        return out
 
 
 class AgreementDraft:

@@ -98,7 +98,9 @@ def _import(lib, handle: bytes, offset: int) -> tuple:
 def _clock(lib, dev, stream) -> int:
     v = C.c_int64()
     with torch.cuda.device(dev):
-        L.check(lib.amusd_device_clock(C.byref(v), stream.cuda_stream))
+        scratch = torch.empty(1, dtype=torch.int64, device=dev)
+        torch.cuda.current_stream(dev).synchronize()
+        L.check(lib.amusd_device_clock(C.byref(v), C.c_void_p(scratch.data_ptr()), stream.cuda_stream))
     return v.value
 
 

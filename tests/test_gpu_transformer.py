@@ -157,10 +157,18 @@ def test_amusd_draft_cut_on_and_off(bf16_pair, monkeypatch):
     for cut in ("0", "1"):
         monkeypatch.setenv("AMUSD_FW_CUT", cut)
         P.engines.clear_sessions()  # the knob is read when the session's graphs are captured
+        cuts = []
         for rho in (0.5, 0.8):
-            res = P.decode_speculative_async(P.AgreementDraft(d, rho), v, PROMPT, cfg)
+            ex = P.CudaAsyncExecutor()
+            res = P.decode_speculative_async(P.AgreementDraft(d, rho), v, PROMPT, cfg, executor=ex)
             assert res.tokens == ar.tokens, (cut, rho)
             res.trace.validate()
+            cuts.append(ex.last_run.info.draft_cuts)   # cumulative per draft model
+        if cut == "1":
+            assert cuts[-1] > cuts0, "the cut arm never cut a draft forward"
+        else:
+            cuts0 = cuts[-1]
+            assert cuts[0] == cuts[-1], "draft forwards were cut with AMUSD_FW_CUT=0"
         # the draft model's own greedy decode after cut forwards: unchanged (no stale
         # split-K accumulators / counters / argmax keys)
         assert P.decode_autoregressive(d, PROMPT, cfg).tokens == d_ar, cut
