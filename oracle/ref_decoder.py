@@ -42,6 +42,9 @@ class TfShape:
     eps: float = 1e-5
     theta: float = 500000.0
     kv_bf16: bool = False
+    # bf16-faithful mode: round activations to bf16 exactly where the tcgen05 kernels do
+    # (normed GEMM inputs bf16(h*g), attention output, SiLU*up product); accumulation fp32
+    act_bf16: bool = False
 
 
 @dataclass
@@ -74,9 +77,12 @@ class RefDecoder:
         x1, x2 = x[..., :half], x[..., half:]
         return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1)
 
+    def _act(self, a):
+        return bf16_round(a) if self.s.act_bf16 else a
+
     def _normed_matmul(self, h, g, W):
         inv = 1.0 / np.sqrt((h * h).mean(axis=1, keepdims=True) + np.float32(self.s.eps))
-        return ((h * g[None, :]) @ W.T) * inv.astype(np.float32)
+        return (self._act(h * g[None, :]) @ W.T) * inv.astype(np.float32)
 
     def _cast_kv(self, a):
         return bf16_round(a) if self.s.kv_bf16 else a
@@ -113,12 +119,12 @@ class RefDecoder:
                 sc = np.exp(sc - sc.max(axis=1, keepdims=True))
                 sc = sc / sc.sum(axis=1, keepdims=True)
                 out[:, hh, :] = sc @ vv[g]
-            h = h + out.reshape(m, H * hd) @ w[p + "wo"].T
-            x = h * w[p + "mlp_norm"][None, :]
+            h = h + self._act(out.reshape(m, H * hd)) @ w[p + "wo"].T
+            x = self._act(h * w[p + "mlp_norm"][None, :])
             inv = (1.0 / np.sqrt((h * h).mean(axis=1, keepdims=True) + np.float32(s.eps))).astype(np.float32)
             gg = (x @ w[p + "wgate"].T) * inv
             uu = (x @ w[p + "wup"].T) * inv
-            a = (gg / (1.0 + np.exp(-gg))) * uu
+            a = self._act((gg / (1.0 + np.exp(-gg))) * uu)
             h = h + a @ w[p + "wdown"].T
         logits = self._normed_matmul(h, w["final_norm"], self.lm)
         self.scratch = (newk, newv)   # the KV this forward produced (ref_models reuses it on advance)

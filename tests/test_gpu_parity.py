@@ -27,7 +27,9 @@ from oracle.ref_models import load_reference, make_models, shape_of
 pytestmark = pytest.mark.gpu
 P = pytest.importorskip("paper_2410_17375_b200")
 
-BF16_LOGIT_TOL = 3e-2   # max |gpu - cpu| / std(cpu logits): bf16 weights/activations/KV vs fp32 CPU
+BF16_LOGIT_TOL = 3e-2   # max |gpu - cpu| / std(cpu logits): bf16 weights/activations/KV vs fp32 CPU (shallow)
+FAITHFUL_TOL = 1e-2     # same, vs the bf16-faithful oracle (act_bf16: fp32 summation order only)
+DEEP_BF16_TOL = 1e-1    # same, vs the pure-fp32 oracle at full depth (16 / 32 layers of bf16 activations)
 PROMPT32 = [(1234 * (i + 7)) % 31990 + 3 for i in range(32)]
 
 
@@ -57,7 +59,10 @@ def _host_ram_gb():
 
 @pytest.mark.parametrize("shape", ["llama_1b", "llama_8b"])
 def test_bench_shapes_vs_cpu_oracle(shape):
-    """Full-depth bench-shape forward (persistent tcgen05 path) vs the CPU fp32 oracle."""
+    """Full-depth bench-shape forward (persistent tcgen05 path) vs the CPU oracle on the same
+    bf16 weights: the bf16-faithful oracle (activations rounded where the kernels round them;
+    only fp32 summation order differs) within FAITHFUL_TOL, the pure-fp32 oracle within
+    DEEP_BF16_TOL (bf16 activation quantisation accumulated over 16 / 32 layers)."""
     import torch
     TC = P.TransformerConfig
     need = {"llama_1b": 12, "llama_8b": 70}[shape]
@@ -65,29 +70,33 @@ def test_bench_shapes_vs_cpu_oracle(shape):
         pytest.skip(f"needs ~{need} GB host RAM for the fp32 oracle")
     cfg = getattr(TC, shape)(max_seq=96)
     m = P.TransformerModel(cfg, seed={"llama_1b": 1, "llama_8b": 0}[shape])
-    rv = RefDecoder(shape_of(cfg, kv_bf16=True), m.host_weights(), tied=cfg.tied)
+    w = m.host_weights()
+    rf = RefDecoder(shape_of(cfg, kv_bf16=True, act_bf16=True), w, tied=cfg.tied)
+    r32 = RefDecoder(shape_of(cfg, kv_bf16=True), w, tied=cfg.tied)
     n = 8
     ar = P.decode_autoregressive(m, PROMPT32, P.DecodeConfig(max_new_tokens=n)).tokens
     st = m.init_state(PROMPT32)
     m.next_token(st)
     gl = m.last_logits(1).numpy()[0]
-    rs = rv.start(PROMPT32)
+    rs, r32s = rf.start(PROMPT32), r32.start(PROMPT32)
     err = float(np.abs(gl - rs.last_logits).max() / rs.last_logits.std())
-    assert err < BF16_LOGIT_TOL, err
+    err32 = float(np.abs(gl - r32s.last_logits).max() / r32s.last_logits.std())
+    print(f"{shape}: max|gpu-cpu|/std: bf16-faithful oracle {err:.2e}, fp32 oracle {err32:.2e}")
+    assert err < FAITHFUL_TOL, err
+    assert err32 < DEEP_BF16_TOL, err32
     cpu, gaps = [], []
     for i in range(n):
         z = np.array(rs.last_logits, dtype=np.float32)
         z[cfg.eos_token] = -np.inf
         top2 = np.sort(z)[-2:]
-        cpu.append(rv.predict(rs))
+        cpu.append(rf.predict(rs))
         gaps.append(float((top2[1] - top2[0]) / rs.last_logits.std()))
-        rv.extend(rs, [ar[i]])        # teacher-forced on the GPU's path: per-position comparison
+        rf.extend(rs, [ar[i]])        # teacher-forced on the GPU's path: per-position comparison
     mism = [(i, ar[i], cpu[i], gaps[i]) for i in range(n) if ar[i] != cpu[i]]
+    print(f"{shape}: AR tokens {n - len(mism)}/{n} equal to the faithful oracle; mismatches {mism}")
     # a mismatch is legitimate only at a near-tie (top-2 gap within the logit tolerance)
-    assert all(g < 2 * BF16_LOGIT_TOL for (_, _, _, g) in mism), mism
-    assert ar[0] == cpu[0] or gaps[0] < 2 * BF16_LOGIT_TOL
-    print(f"{shape}: logit err {err:.2e}; tokens {n - len(mism)}/{n} equal; mismatches {mism}")
-    del m
+    assert all(g < 2 * FAITHFUL_TOL for (_, _, _, g) in mism), mism
+    del m, w, rf, r32
     P.engines.clear_sessions()
     torch.cuda.empty_cache()
 
