@@ -243,6 +243,9 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
             "rollbacks": statistics.mean(i.rollbacks for i in stats),
             "drafted": statistics.mean(i.drafted for i in stats),
         }
+    variants = None
+    if not args.no_extras and world == 1:
+        variants = engine_variants(args, P, L, DeviceSession, finalize_tokens, dm, vm, prompt, canon, N, Plen, ref_tokens)
     if args.no_extras:
         return {"results": results, "roofline": None, "e2e": None, "clocks": sampler.summary() if sampler else None,
                 "vm": vm, "dm": dm, "prompt": prompt, "canon": canon.tolist(), "vcfg": vcfg, "dcfg": dcfg}
@@ -307,9 +310,55 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
         e2e = {"value": round(e2e_toks / (sum(e2e_ms) / 1000.0), 2), "unit": "tokens/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "includes": "prefill of both models + graph launch + V/trace read-back + trace merge"}
+    calib = None
+    if world == 1:   # section 8(f)3: measured latencies -> the reference's own simulator
+        try:
+            from paper_2410_17375_b200 import calibrate as CB
+            calib = CB.calibrate(dm, vm, ctx=Plen + N // 2, n_tokens=N)
+            calib["measured_colocated_1gpu"] = {"ar": round(results["ar"]["tokens_per_s"], 3),
+                                                "sync_k4": round(results["sync"]["tokens_per_s"], 3),
+                                                "amusd": round(results["amusd"]["tokens_per_s"], 3)}
+        except Exception as exc:  # reference not installed: say so, never fake a prediction
+            calib = {"unavailable": f"{type(exc).__name__}: {exc}"}
     return {"results": results, "roofline": roofline, "e2e": e2e, "clocks": sampler.summary() if sampler else None,
             "vm": vm, "dm": dm, "prompt": prompt, "canon": canon.tolist(), "vcfg": vcfg, "dcfg": dcfg,
-            "first_logits": first_logits}
+            "first_logits": first_logits, "variants": variants, "calibration": calib}
+
+
+def engine_variants(args, P, L, DeviceSession, finalize_tokens, dm, vm, prompt, canon, N, Plen, ref_tokens):
+    """SURVEY.md section 7.3.2 reporting: AMUSD and sync-SD at rho=0.9 as well, and the sync-SD
+    k sweep (best k next to the reference default k=4).  1 warm-up + 2 timed decodes each,
+    device-timed, tokens checked against the AR path like the headline engines."""
+    def timed(sess, eng, n=2):
+        sess.run(eng, prompt)
+        ms, toks, info = 0.0, 0, []
+        for _ in range(n):
+            sess.prepare(prompt)
+            start, end = sess.launch(eng)
+            out = sess.collect(start, end)
+            tokens, _ = finalize_tokens(out.verified, vm.eos_token, N)
+            if tokens != ref_tokens:
+                raise SystemExit("variant output differs from the AR oracle -- parity broken")
+            ms += out.device_ms
+            toks += len(tokens)
+            info.append(out.info)
+        return {"tokens_per_s": round(toks / (ms / 1000.0), 3), "verify_steps": statistics.mean(i.verify_steps for i in info),
+                "rollbacks": statistics.mean(i.rollbacks for i in info)}
+    out = {}
+    d9 = P.AgreementDraft(dm, 0.9, coin_seed=1234)
+    c4 = P.DecodeConfig(max_new_tokens=N, draft_window_k=args.k, max_draft_lead=args.lead or None)
+    out["rho0.9"] = {"sync_k4": timed(DeviceSession(d9, vm, Plen, c4, canon=canon), L.ENGINE_SYNC),
+                     "amusd": timed(DeviceSession(d9, vm, Plen, c4, canon=canon, max_window=args.window),
+                                    L.ENGINE_ASYNC)}
+    for rho, d in ((args.rho, P.AgreementDraft(dm, args.rho, coin_seed=1234)), (0.9, d9)):
+        sweep = {}
+        for k in (2, 3, 4, 5, 6, 8):
+            ck = P.DecodeConfig(max_new_tokens=N, draft_window_k=k, max_draft_lead=args.lead or None)
+            sweep[k] = timed(DeviceSession(d, vm, Plen, ck, canon=canon), L.ENGINE_SYNC)["tokens_per_s"]
+        best = max(sweep, key=sweep.get)
+        out[f"rho{rho}"] = dict(out.get(f"rho{rho}", {}), sync_k_sweep=sweep, sync_best={"k": best, "tokens_per_s": sweep[best]})
+    P.engines.clear_sessions()
+    return out
 
 
 # --------------------------------------------------------------- CPU arm
@@ -421,10 +470,15 @@ def cpu_leg(args, out):
     fd = RefDecoder(shape_of(out["dcfg"], kv_bf16=True, act_bf16=True), wd, tied=out["dcfg"].tied)
     prompt = out["prompt"]
     par = {}
-    for key, f, r in (("verify", fv, rv), ("draft", fd, rd)):
+    for key, f, r, c, w in (("verify", fv, rv, out["vcfg"], wv), ("draft", fd, rd, out["dcfg"], wd)):
         gl = out["first_logits"][key]
         fl, cl = f.start(prompt).last_logits, r.start(prompt).last_logits
+        # fp32 noise floor: the same faithful oracle with float64 accumulation (tests/test_gpu_parity.py)
+        f64 = RefDecoder(shape_of(c, kv_bf16=True, act_bf16=True, acc64=True), w, tied=c.tied)
+        hl = f64.start(prompt).last_logits
+        del f64
         par[f"{key}_logit_err_faithful"] = round(float(np.abs(gl - fl).max() / fl.std()), 6)
+        par[f"{key}_noise_floor"] = round(float(np.abs(hl - fl).max() / fl.std()), 6)
         par[f"{key}_logit_err_fp32"] = round(float(np.abs(gl - cl).max() / cl.std()), 6)
         par[f"{key}_argmax_equal"] = bool(int(np.argmax(gl)) == int(np.argmax(fl)))
     gpu = out["canon"][len(prompt):len(prompt) + args.cpu_tokens]
@@ -434,8 +488,9 @@ def cpu_leg(args, out):
         cpu_tok.append(fv.predict(st))
         fv.extend(st, [t])
     match = sum(int(a == b) for a, b in zip(cpu_tok, gpu))
-    par.update({"tolerance": "max|gpu-cpu|/std(cpu logits): <= 1e-2 vs the bf16-faithful oracle, <= 1e-1 vs "
-                             "the fp32 oracle (tests/test_gpu_parity.py)",
+    par.update({"tolerance": "max|gpu-cpu|/std(cpu logits): <= 2x the noise floor (|faithful fp32 - faithful "
+                             "float64-accumulated|/std) vs the bf16-faithful oracle, <= 2e-1 vs the pure fp32 "
+                             "oracle (tests/test_gpu_parity.py)",
                 "ar_tokens_cpu_faithful": cpu_tok, "ar_tokens_gpu": gpu, "ar_tokens_match": f"{match}/{len(gpu)}"})
     del fv, fd
     s = reference_cpu_run(rv, rd, prompt, args.rho, args.cpu_tokens, k=args.k)
@@ -489,6 +544,7 @@ def main():
                 "ar": {k: round(v, 3) for k, v in ar.items()},
                 "speedup_vs_sync": round(a["tokens_per_s"] / sy["tokens_per_s"], 3),
                 "speedup_vs_ar": round(a["tokens_per_s"] / ar["tokens_per_s"], 3),
+                "variants": out.get("variants"), "calibration": out.get("calibration"),
                 "roofline": out["roofline"], "cpu_baseline": cpu, "parity": parity, "e2e": out["e2e"],
                 "gpu_launches": int(a["gpu_launches"]), "clocks": out["clocks"],
             }

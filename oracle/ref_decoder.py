@@ -45,6 +45,9 @@ class TfShape:
     # bf16-faithful mode: round activations to bf16 exactly where the tcgen05 kernels do
     # (normed GEMM inputs bf16(h*g), attention output, SiLU*up product); accumulation fp32
     act_bf16: bool = False
+    # float64 accumulation in every matmul (rounded to fp32 at the same points): a second
+    # summation order, i.e. the fp32 noise floor the GPU parity tolerance is measured against
+    acc64: bool = False
 
 
 @dataclass
@@ -80,9 +83,14 @@ class RefDecoder:
     def _act(self, a):
         return bf16_round(a) if self.s.act_bf16 else a
 
+    def _mm(self, x, W):
+        if self.s.acc64:
+            return (x.astype(np.float64) @ W.T.astype(np.float64)).astype(np.float32)
+        return x @ W.T
+
     def _normed_matmul(self, h, g, W):
         inv = 1.0 / np.sqrt((h * h).mean(axis=1, keepdims=True) + np.float32(self.s.eps))
-        return (self._act(h * g[None, :]) @ W.T) * inv.astype(np.float32)
+        return self._mm(self._act(h * g[None, :]), W) * inv.astype(np.float32)
 
     def _cast_kv(self, a):
         return bf16_round(a) if self.s.kv_bf16 else a
@@ -119,13 +127,13 @@ class RefDecoder:
                 sc = np.exp(sc - sc.max(axis=1, keepdims=True))
                 sc = sc / sc.sum(axis=1, keepdims=True)
                 out[:, hh, :] = sc @ vv[g]
-            h = h + self._act(out.reshape(m, H * hd)) @ w[p + "wo"].T
+            h = h + self._mm(self._act(out.reshape(m, H * hd)), w[p + "wo"])
             x = self._act(h * w[p + "mlp_norm"][None, :])
             inv = (1.0 / np.sqrt((h * h).mean(axis=1, keepdims=True) + np.float32(s.eps))).astype(np.float32)
-            gg = (x @ w[p + "wgate"].T) * inv
-            uu = (x @ w[p + "wup"].T) * inv
+            gg = self._mm(x, w[p + "wgate"]) * inv
+            uu = self._mm(x, w[p + "wup"]) * inv
             a = self._act((gg / (1.0 + np.exp(-gg))) * uu)
-            h = h + a @ w[p + "wdown"].T
+            h = h + self._mm(a, w[p + "wdown"])
         logits = self._normed_matmul(h, w["final_norm"], self.lm)
         self.scratch = (newk, newv)   # the KV this forward produced (ref_models reuses it on advance)
         if commit:

@@ -240,8 +240,8 @@ def make_models(S=None):
     return DecoderModel, CoinDraftModel, ShimExecutor
 
 
-def shape_of(cfg, kv_bf16: bool, act_bf16: bool = False) -> TfShape:
+def shape_of(cfg, kv_bf16: bool, act_bf16: bool = False, acc64: bool = False) -> TfShape:
     """TfShape of a paper_2410_17375_b200.TransformerConfig (duck-typed)."""
     return TfShape(cfg.vocab_size, cfg.d_model, cfg.n_layers, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.ffn,
                    eos=cfg.eos_token, exclude_eos=cfg.exclude_eos, eps=cfg.norm_eps, theta=cfg.rope_theta,
-                   kv_bf16=kv_bf16, act_bf16=act_bf16)
+                   kv_bf16=kv_bf16, act_bf16=act_bf16, acc64=acc64)
