@@ -95,6 +95,11 @@ def _import(lib, handle: bytes, offset: int) -> tuple:
     return ptr.value, base.value
 
 
+# The last distributed run of this process: its actor's loop iterations and kernels per step
+# (bench.py's gpu_launches).
+last_run: dict = {}
+
+
 def _clock(lib, dev, stream) -> int:
     v = C.c_int64()
     with torch.cuda.device(dev):
@@ -262,6 +267,9 @@ def decode_speculative_async_split(model, prompt: Sequence[int], config: DecodeC
             st.synchronize()
         ms = start.elapsed_time(end)
         info, rows, verified = _collect(half)
+        last_run.clear()
+        last_run.update({"role": role, "iters": info.draft_iters if role == "draft" else info.verify_iters,
+                         "kernels_per_step": half.session.kernels_per_step(half.engine)[0 if role == "draft" else 1]})
         mine = rows[0] if role == "draft" else rows[1]
         if role == "draft":  # express the draft events on the verify GPU's clock
             shift = peer_clk - clk
