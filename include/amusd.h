@@ -112,6 +112,45 @@ int amusd_scripted_create(amusd_model** out, const int32_t* script, int script_l
 
 int amusd_model_destroy(amusd_model* m);
 
+/* Tensor-parallel shard of a transformer (BASELINE config 4: the verify model
+ * sharded over tp_size GPUs; not in the reference, which has no transformer).
+ * The amusd_tf_config passed with it describes the SHARD: n_heads / n_kv_heads
+ * / ffn / vocab are this rank's slice -- whole KV groups (QKV column-parallel,
+ * O row-parallel), whole gate/up features (gate/up column-parallel, down
+ * row-parallel), whole 128-row vocab tiles of the LM head.  The embedding and
+ * the norms are replicated.  Only the persistent forward runs shards: the O and
+ * down partials are red.added into EVERY rank's int64 split-K accumulators
+ * over peer memory (the allreduce fused into the GEMM epilogue) and the LM-head
+ * argmax keys into every rank's, so every rank computes the same predictions --
+ * bit-identical to the unsharded forward (the shard takes the unsharded
+ * model's split-K chunking).  Replaces nothing in the reference: its only
+ * parallelism is the two actor threads (engines.py:448-459). */
+typedef struct {
+  int tp_rank, tp_size;        /* 2 <= tp_size <= 8 */
+  int n_heads_full, n_kv_heads_full, ffn_full;  /* the unsharded model */
+  int vocab_offset;            /* global vocab id of this shard's first LM-head row */
+  int vocab_total;             /* embedding rows (valid token ids) */
+} amusd_tp_shard;
+/* One rank's cross-rank words (device pointers, valid in the exporting process;
+ * translate through CUDA IPC for another process). */
+typedef struct {
+  void* ws;        /* int64 split-K accumulators */
+  void* tile_cnt;  /* split-K tile counters */
+  void* best;      /* argmax keys */
+  void* sched;     /* schedule block (LM-head arrival counter) */
+  int lm_items;    /* LM-head work items of this rank */
+  int pad;
+} amusd_tp_peer;
+size_t amusd_tf_shard_state_bytes(const amusd_tf_config* cfg, const amusd_tp_shard* shard);
+int amusd_tf_create_shard(amusd_model** out, const amusd_tf_config* cfg, const amusd_tp_shard* shard,
+                          const amusd_tf_weights* w, void* state, size_t state_bytes);
+int amusd_tp_export(amusd_model* m, amusd_tp_peer* out);
+/* All ranks' words in rank order (n == tp_size, this rank's own included);
+ * required before the shard's first forward. */
+int amusd_tp_connect(amusd_model* m, const amusd_tp_peer* peers, int n);
+/* One process driving several GPUs: let `device` load/store/atomically update `peer`'s HBM. */
+int amusd_peer_enable(int device, int peer);
+
 /* Forward implementation of a bf16 tensor-core-shaped transformer (perf A/B
  * and parity tests; not in the reference, whose models are Python mocks):
  * 0 = persistent tcgen05 forward (default, one launch per forward),
@@ -126,6 +165,11 @@ int amusd_model_release_row_major(amusd_model* m);
 /* Perf analysis only: run amusd_time_forward's persistent launches on `sms`
  * SMs (0 = all), e.g. the share a co-located session gives the model. */
 int amusd_model_set_grid(amusd_model* m, int sms);
+/* Cap every persistent launch of the model (API forwards and non-co-located
+ * engine loops) at `sms` CTAs (0 = all SMs).  Ranks of a tensor-parallel group
+ * emulated on ONE GPU need this: their forwards wait on each other, so their
+ * grids must be co-resident (sum <= SM count). */
+int amusd_model_set_max_grid(amusd_model* m, int sms);
 /* Perf analysis only: record a per-work-item timeline of the persistent
  * forward into a device buffer (64 bytes per item; NULL disables). */
 int amusd_model_set_timeline(amusd_model* m, void* buf, size_t bytes);
@@ -171,6 +215,13 @@ int amusd_session_create(amusd_session** out, amusd_model* draft, amusd_model* v
                          const amusd_session_desc* d, void* mem, size_t mem_bytes,
                          void* mb_local, void* mb_peer);
 int amusd_session_destroy(amusd_session* s);
+/* Tensor-parallel verify group (BASELINE config 4): the leader rank's
+ * k_verify_begin snapshots the draft window and pushes the step control into
+ * every follower's inbox (peer memory); followers run the same loop on it.
+ * role 0 = none, 1 = leader (followers = the followers' inboxes, n <= 7),
+ * 2 = follower.  Sessions of one group must run the same engine. */
+int amusd_session_tp_inbox(amusd_session* s, void** out);
+int amusd_session_set_tp(amusd_session* s, int role, void* const* followers, int n);
 
 /* Reset the mailbox, coin chain and trace rings for a fresh run; the models
  * must already hold init_state(prompt).  Prompt is a host buffer. */

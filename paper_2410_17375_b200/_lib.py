@@ -53,6 +53,16 @@ class RunInfo(C.Structure):
                                          "draft_iters", "verify_iters", "draft_cuts")]
 
 
+class TpShard(C.Structure):  # amusd_tp_shard
+    _fields_ = [(n, C.c_int) for n in ("tp_rank", "tp_size", "n_heads_full", "n_kv_heads_full", "ffn_full",
+                                         "vocab_offset", "vocab_total")]
+
+
+class TpPeer(C.Structure):  # amusd_tp_peer
+    _fields_ = [("ws", C.c_void_p), ("tile_cnt", C.c_void_p), ("best", C.c_void_p), ("sched", C.c_void_p),
+                ("lm_items", C.c_int), ("pad", C.c_int)]
+
+
 class TraceEvent(C.Structure):
     _fields_ = [("t_ns", C.c_int64), ("busy_ns", C.c_int64), ("kind", C.c_int32), ("pos_lo", C.c_int32),
                 ("pos_hi", C.c_int32), ("draft_accepted", C.c_int32)]
@@ -70,6 +80,14 @@ SIGNATURES = [
     ("amusd_scripted_state_bytes", _SZ, [_I, _I]),
     ("amusd_scripted_create", _I, [_P(_VP), _P(C.c_int32), _I, _I, _I, _I, _I, _VP, _SZ, _VP]),
     ("amusd_model_destroy", _I, [_VP]),
+    ("amusd_tf_shard_state_bytes", _SZ, [_P(TfConfig), _P(TpShard)]),
+    ("amusd_tf_create_shard", _I, [_P(_VP), _P(TfConfig), _P(TpShard), _P(TfWeights), _VP, _SZ]),
+    ("amusd_tp_export", _I, [_VP, _P(TpPeer)]),
+    ("amusd_tp_connect", _I, [_VP, _P(TpPeer), _I]),
+    ("amusd_model_set_max_grid", _I, [_VP, _I]),
+    ("amusd_peer_enable", _I, [_I, _I]),
+    ("amusd_session_tp_inbox", _I, [_VP, _P(_VP)]),
+    ("amusd_session_set_tp", _I, [_VP, _I, _P(_VP), _I]),
     ("amusd_model_set_path", _I, [_VP, _I]),
     ("amusd_model_set_grid", _I, [_VP, _I]),
     ("amusd_model_release_row_major", _I, [_VP]),

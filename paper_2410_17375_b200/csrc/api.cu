@@ -125,10 +125,14 @@ struct amusd_model {
   const int* fw_ab_done = nullptr;
   size_t fw_ws_floats = 0, fw_cnt_ints = 0, fw_attn_cnt_ints = 0;  // cut cleanup extents
   int grid_override = 0;            // amusd_model_set_grid: SMs of amusd_time_forward launches (0 = all)
+  int max_grid = 0;                 // amusd_model_set_max_grid: cap of every persistent launch (0 = all SMs)
   int path = AMUSD_PATH_PERSISTENT;
   bool row_major = true;  // row-major layer weights still valid (amusd_model_release_row_major)
   long long* fw_dbg = nullptr;  // optional per-item timeline (amusd_model_set_timeline)
   int fw_dbg_items = 0;
+  // tensor-parallel shard (amusd_tf_create_shard): tp.tp_size == 0 when not sharded
+  amusd_tp_shard tp{};
+  bool tp_connected = false;
 };
 
 static int env_int(const char* name, int dflt) {
@@ -147,6 +151,8 @@ static int fw_units() {
   return v;
 }
 static int num_sms() { return device_sms(); }
+// SMs of this model's persistent launches outside co-located AMUSD (amusd_model_set_max_grid).
+static int model_sms(const amusd_model* m) { return m->max_grid > 0 ? std::min(m->max_grid, num_sms()) : num_sms(); }
 // Deepest weight ring that fits `per_sm` CTAs on one SM (227 KB smem per SM).
 static int fw_max_stages(const amusd_tf_config& c, int per_sm) {
   const int group = c.n_heads / c.n_kv_heads;
@@ -167,15 +173,21 @@ static bool tc_shapes_ok(const amusd_tf_config* c) {
 }
 
 // Split-K workspace sizes of a config (dry run of build_kinds without pointers).
-static void fw_sizes(const amusd_tf_config* c, size_t* ws_floats, int* cnt_ints, int* max_tiles) {
+static void view_shard(fw::ModelView* v, const amusd_tp_shard* sh) {
+  if (!sh || sh->tp_size < 2) return;
+  v->tp = sh->tp_size; v->H_full = sh->n_heads_full; v->KV_full = sh->n_kv_heads_full; v->ffn_full = sh->ffn_full;
+}
+static bool fw_sizes(const amusd_tf_config* c, const amusd_tp_shard* sh, size_t* ws_floats, int* cnt_ints,
+                     int* max_tiles) {
   fw::ModelView v{};
   v.d = c->d_model; v.H = c->n_heads; v.KV = c->n_kv_heads; v.hd = c->head_dim; v.ffn = c->ffn; v.vocab = c->vocab;
   v.L = c->n_layers; v.S = c->max_seq;
+  view_shard(&v, sh);
   fw::FwArgs a{};
-  fw::build_kinds(v, fw_units(), &a, ws_floats, cnt_ints, max_tiles);
+  return fw::build_kinds(v, fw_units(), &a, ws_floats, cnt_ints, max_tiles);
 }
 
-static size_t tf_carve(const amusd_tf_config* c, void* base, amusd_model* m) {
+static size_t tf_carve(const amusd_tf_config* c, void* base, amusd_model* m, const amusd_tp_shard* sh = nullptr) {
   Carver cv(base);
   const size_t wsz = c->dtype == AMUSD_BF16 ? 2 : 4;
   const int ncols = (c->n_heads + 2 * c->n_kv_heads) * c->head_dim;
@@ -229,7 +241,7 @@ static size_t tf_carve(const amusd_tf_config* c, void* base, amusd_model* m) {
     int mt;
     size_t wsf;
     int cints;
-    fw_sizes(c, &wsf, &cints, &mt);
+    fw_sizes(c, sh, &wsf, &cints, &mt);
     fsched = cv.take<int>(fw::sched_ints(c->n_layers));
     fbest = cv.take<unsigned long long>(KMAX);
     fws = cv.take<float>(std::max<size_t>(wsf, 1));
@@ -249,7 +261,7 @@ static size_t tf_carve(const amusd_tf_config* c, void* base, amusd_model* m) {
     if (tc) {
       size_t wsf;
       int cints, mt;
-      fw_sizes(c, &wsf, &cints, &mt);
+      fw_sizes(c, sh, &wsf, &cints, &mt);
       m->fw_ws_floats = std::max<size_t>(wsf, 1);
       m->fw_cnt_ints = (size_t)cints;
       m->fw_attn_cnt_ints = (size_t)c->n_kv_heads * KMAX * fw::kCounterInts;
@@ -409,6 +421,8 @@ static bool use_tc(const amusd_model* m, int nr) {
 // The whole forward as one persistent launch (forward_tc.cu).
 static int fw_forward(amusd_model* m, StepCtl* ctl, cudaStream_t st, bool want_logits) {
   const amusd_tf_config& c = m->cfg;
+  if (m->tp.tp_size > 1 && !m->tp_connected)
+    return fail(AMUSD_ERR_INVALID_INPUT, "tensor-parallel shard used before amusd_tp_connect");
   fw::FwArgs a = m->fw_args;
   if (m->fw_part_ok && m->fw_grid < num_sms()) {  // co-located AMUSD draft: larger work items
     if (m->fw_part_grid != m->fw_grid) {
@@ -485,21 +499,37 @@ int amusd_abi_version(void) { return AMUSD_ABI_VERSION; }
 const char* amusd_last_error(void) { return g_err.c_str(); }
 
 size_t amusd_tf_state_bytes(const amusd_tf_config* cfg) { return cfg ? tf_carve(cfg, nullptr, nullptr) : 0; }
+size_t amusd_tf_shard_state_bytes(const amusd_tf_config* cfg, const amusd_tp_shard* sh) {
+  return cfg ? tf_carve(cfg, nullptr, nullptr, sh) : 0;
+}
 
-int amusd_tf_create(amusd_model** out, const amusd_tf_config* cfg, const amusd_tf_weights* w, void* state,
-                    size_t state_bytes) {
+}  // extern "C"
+
+static int tf_create(amusd_model** out, const amusd_tf_config* cfg, const amusd_tp_shard* sh,
+                     const amusd_tf_weights* w, void* state, size_t state_bytes) {
   if (!out || !cfg || !w || !state) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
   const amusd_tf_config& c = *cfg;
   if (c.vocab < 2 || c.d_model <= 0 || c.n_layers <= 0 || c.n_layers > AMUSD_MAX_LAYERS || c.n_heads <= 0 ||
       c.n_kv_heads <= 0 || c.n_heads % c.n_kv_heads || c.head_dim % 8 || c.head_dim > 256 || c.ffn <= 0 ||
       c.max_seq < 2)
     return fail(AMUSD_ERR_INVALID_INPUT, "invalid transformer config");
-  if (!(0 <= c.eos_token && c.eos_token < c.vocab))
+  const int vocab_total = sh ? sh->vocab_total : c.vocab;
+  if (!(0 <= c.eos_token && c.eos_token < vocab_total))
     return fail(AMUSD_ERR_INVALID_INPUT, "eos_token out of range");  // models.py:98-101
+  if (sh) {
+    if (sh->tp_size < 2 || sh->tp_size > fw::kMaxTp || sh->tp_rank < 0 || sh->tp_rank >= sh->tp_size)
+      return fail(AMUSD_ERR_INVALID_INPUT, "tp_rank / tp_size out of range (2 <= tp_size <= 8)");
+    if (sh->n_kv_heads_full <= 0 || sh->n_heads_full % sh->n_kv_heads_full ||
+        sh->n_heads_full / sh->n_kv_heads_full != c.n_heads / c.n_kv_heads || c.n_kv_heads > sh->n_kv_heads_full ||
+        c.ffn > sh->ffn_full || sh->vocab_offset < 0 || sh->vocab_offset + c.vocab > sh->vocab_total)
+      return fail(AMUSD_ERR_INVALID_INPUT, "tensor-parallel shard inconsistent with the unsharded model");
+    if (c.dtype != AMUSD_BF16 || !c.use_tensor_cores || !fw_enabled())
+      return fail(AMUSD_ERR_UNSUPPORTED, "tensor-parallel shards run on the persistent bf16 tcgen05 forward only");
+  }
   if (c.d_model % 256 || c.ffn % 256 || (c.n_heads * c.head_dim) % 256)
     return fail(AMUSD_ERR_UNSUPPORTED, "d_model, ffn and n_heads*head_dim must be multiples of 256");
   if (c.dtype != AMUSD_F32 && c.dtype != AMUSD_BF16) return fail(AMUSD_ERR_INVALID_INPUT, "bad dtype");
-  if (state_bytes < amusd_tf_state_bytes(cfg)) return fail(AMUSD_ERR_INVALID_INPUT, "state buffer too small");
+  if (state_bytes < tf_carve(cfg, nullptr, nullptr, sh)) return fail(AMUSD_ERR_INVALID_INPUT, "state buffer too small");
   {
     const int group = c.n_heads / c.n_kv_heads;
     if (!(c.head_dim == 64 || c.head_dim == 128) || !(group == 2 || group == 4 || group == 8))
@@ -509,11 +539,16 @@ int amusd_tf_create(amusd_model** out, const amusd_tf_config* cfg, const amusd_t
   m->kind = 0;
   m->cfg = c;
   m->w = *w;
-  m->vocab = c.vocab;
+  m->vocab = vocab_total;  // token ids (a shard's LM head covers cfg.vocab of them)
   m->eos = c.eos_token;
   m->exclude_eos = c.exclude_eos;
   m->max_seq = c.max_seq;
-  tf_carve(cfg, state, m);
+  if (sh) m->tp = *sh;
+  tf_carve(cfg, state, m, sh);
+  if (sh && !m->tc) {
+    delete m;
+    return fail(AMUSD_ERR_UNSUPPORTED, "tensor-parallel shard shape does not fit the tcgen05 tiles");
+  }
   if (m->tc) {
     const int d = c.d_model, ncols = (c.n_heads + 2 * c.n_kv_heads) * c.head_dim, hh = c.n_heads * c.head_dim;
     bool ok = true;
@@ -551,12 +586,18 @@ int amusd_tf_create(amusd_model** out, const amusd_tf_config* cfg, const amusd_t
       v.wt_lm = m->wt_lm; v.norms = m->fw_norms;
       v.h = m->h; v.qkv = m->qkv; v.xa = m->xa_b; v.act_b = m->act_b;
       v.xb = m->fw_xb; v.ssp = m->ssp; v.sspb = m->fw_sspb;
+      view_shard(&v, sh);
       size_t wsf;
       int mt, cints;
-      fw::build_kinds(v, fw_units(), &m->fw_args, &wsf, &cints, &mt);
+      if (!fw::build_kinds(v, fw_units(), &m->fw_args, &wsf, &cints, &mt)) {
+        delete m;
+        return fail(AMUSD_ERR_UNSUPPORTED, "tensor-parallel shard: a rank's O / down K slice is not a whole number of "
+                                           "the unsharded model's split-K chunks (set AMUSD_FW_UNITS_O / _DOWN)");
+      }
+      if (sh) { m->fw_args.vocab_off = sh->vocab_offset; m->fw_args.tp = 1; }  // tp = n at amusd_tp_connect
       m->fw_view = v;
       m->fw_ready = e == cudaSuccess && c.max_seq <= fw::max_positions();  // else the per-kernel path
-      m->fw_grid = num_sms();
+      m->fw_grid = model_sms(m);
       m->fw_stages = env_int("AMUSD_FW_STAGES", fw_max_stages(c, 1));
     }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -570,7 +611,69 @@ int amusd_tf_create(amusd_model** out, const amusd_tf_config* cfg, const amusd_t
                                       (e != cudaSuccess ? cudaGetErrorString(e) : "cuTensorMapEncodeTiled"));
     }
   }
+  if (sh && !m->fw_ready) {
+    delete m;
+    return fail(AMUSD_ERR_UNSUPPORTED, "tensor-parallel shard needs the persistent forward (max_seq too long?)");
+  }
   *out = m;
+  return AMUSD_OK;
+}
+
+extern "C" {
+
+int amusd_tf_create(amusd_model** out, const amusd_tf_config* cfg, const amusd_tf_weights* w, void* state,
+                    size_t state_bytes) {
+  return tf_create(out, cfg, nullptr, w, state, state_bytes);
+}
+int amusd_tf_create_shard(amusd_model** out, const amusd_tf_config* cfg, const amusd_tp_shard* shard,
+                          const amusd_tf_weights* w, void* state, size_t state_bytes) {
+  if (!shard) return fail(AMUSD_ERR_INVALID_INPUT, "null shard");
+  return tf_create(out, cfg, shard, w, state, state_bytes);
+}
+
+int amusd_peer_enable(int device, int peer) {
+  if (device == peer) return AMUSD_OK;
+  int ok = 0;
+  CUDA_TRY(cudaDeviceCanAccessPeer(&ok, device, peer));
+  if (!ok) return fail(AMUSD_ERR_UNSUPPORTED, "no peer access between the two GPUs");
+  int cur = 0;
+  CUDA_TRY(cudaGetDevice(&cur));
+  CUDA_TRY(cudaSetDevice(device));
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) { cudaGetLastError(); e = cudaSuccess; }
+  cudaSetDevice(cur);
+  CUDA_TRY(e);
+  return AMUSD_OK;
+}
+
+int amusd_tp_export(amusd_model* m, amusd_tp_peer* out) {
+  if (!m || !out) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  if (m->kind != 0 || m->tp.tp_size < 2) return fail(AMUSD_ERR_INVALID_INPUT, "not a tensor-parallel shard");
+  *out = amusd_tp_peer{};
+  out->ws = m->fw_ws; out->tile_cnt = m->fw_tile_cnt; out->best = m->fw_best; out->sched = m->fw_sched;
+  out->lm_items = m->fw_args.g[fw::kGLm].nitems;
+  return AMUSD_OK;
+}
+
+int amusd_tp_connect(amusd_model* m, const amusd_tp_peer* peers, int n) {
+  if (!m || !peers) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  if (m->kind != 0 || m->tp.tp_size < 2) return fail(AMUSD_ERR_INVALID_INPUT, "not a tensor-parallel shard");
+  if (n != m->tp.tp_size) return fail(AMUSD_ERR_INVALID_INPUT, "need one peer entry per rank (n == tp_size)");
+  if (peers[m->tp.tp_rank].ws != (void*)m->fw_ws || peers[m->tp.tp_rank].sched != (void*)m->fw_sched)
+    return fail(AMUSD_ERR_INVALID_INPUT, "peers[tp_rank] must be this shard's own words");
+  int lm = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!peers[i].ws || !peers[i].tile_cnt || !peers[i].best || !peers[i].sched || peers[i].lm_items < 1)
+      return fail(AMUSD_ERR_INVALID_INPUT, "incomplete peer entry");
+    m->fw_args.peer_ws[i] = (unsigned long long*)peers[i].ws;
+    m->fw_args.peer_cnt[i] = (int*)peers[i].tile_cnt;
+    m->fw_args.peer_best[i] = (unsigned long long*)peers[i].best;
+    m->fw_args.peer_sched[i] = (int*)peers[i].sched;
+    lm += peers[i].lm_items;
+  }
+  m->fw_args.tp = n;
+  m->fw_args.lm_items_total = lm;
+  m->tp_connected = true;
   return AMUSD_OK;
 }
 
@@ -673,6 +776,14 @@ int amusd_model_release_row_major(amusd_model* m) {
     m->w.wqkv[l] = m->w.wo[l] = m->w.wgate[l] = m->w.wup[l] = m->w.wdown[l] = nullptr;
   if (m->w.lm_head != m->w.embed) m->w.lm_head = nullptr;
   m->row_major = false;
+  return AMUSD_OK;
+}
+
+int amusd_model_set_max_grid(amusd_model* m, int sms) {
+  if (!m || sms < 0) return fail(AMUSD_ERR_INVALID_INPUT, "bad argument");
+  if (m->kind != 0) return AMUSD_OK;
+  m->max_grid = sms;
+  if (m->fw_ready) m->fw_grid = model_sms(m);
   return AMUSD_OK;
 }
 
@@ -870,7 +981,7 @@ int amusd_last_logits(amusd_model* m, float* out, int rows, void* stream) {
   if (!m || !out) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
   if (m->kind != 0) return fail(AMUSD_ERR_UNSUPPORTED, "logits exist only for transformer models");
   rows = std::min(rows, m->last_rows);
-  CUDA_TRY(cudaMemcpyAsync(out, m->logits, sizeof(float) * (size_t)rows * m->vocab, cudaMemcpyDeviceToHost,
+  CUDA_TRY(cudaMemcpyAsync(out, m->logits, sizeof(float) * (size_t)rows * m->cfg.vocab, cudaMemcpyDeviceToHost,
                            (cudaStream_t)stream));
   CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
   return AMUSD_OK;
@@ -895,6 +1006,11 @@ struct amusd_session {
   cudaStream_t capture = nullptr;
   cudaGraphExec_t exec[5][2] = {};
   bool use_pdl = true;
+  // tensor-parallel verify group (amusd_session_set_tp): 1 leader, 2 follower
+  int tp_role = 0;
+  TpInbox* tp_inbox = nullptr;  // this session's inbox (carved; used when a follower)
+  TpInbox* tp_out[kMaxTpOut] = {};
+  int tp_nout = 0;
 };
 
 static int mailbox_cap(const amusd_session_desc* d) { return d->max_new_tokens + 4 * KMAX + 64; }
@@ -910,7 +1026,9 @@ static size_t session_carve(const amusd_session_desc* d, int coin_cap, int promp
   unsigned long long* hash = cv.take<unsigned long long>(coin_cap + 2);
   unsigned char* onpath = cv.take<unsigned char>(coin_cap + 2);
   int* prompt = cv.take<int>(prompt_cap);
+  TpInbox* inbox = cv.take<TpInbox>(1);
   if (s) {
+    s->tp_inbox = inbox;
     s->dctl = dctl; s->vctl = vctl;
     s->dtrace = TraceDev{dev, counts, d->trace_cap};
     s->vtrace = TraceDev{vev, counts + 1, d->trace_cap};
@@ -941,6 +1059,12 @@ static ProtoArgs make_args(amusd_session* s) {
   a.coin = s->coin;
   a.jitter_ns = s->d.jitter_ns;
   a.jitter_seed = s->d.jitter_seed;
+  if (s->tp_role == 1) {
+    for (int i = 0; i < s->tp_nout; ++i) a.tp_out[i] = s->tp_out[i];
+    a.tp_nout = s->tp_nout;
+  } else if (s->tp_role == 2) {
+    a.tp_in = s->tp_inbox;
+  }
   return a;
 }
 
@@ -999,6 +1123,27 @@ int amusd_session_create(amusd_session** out, amusd_model* draft, amusd_model* v
   return AMUSD_OK;
 }
 
+int amusd_session_tp_inbox(amusd_session* s, void** out) {
+  if (!s || !out) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
+  *out = s->tp_inbox;
+  return AMUSD_OK;
+}
+
+int amusd_session_set_tp(amusd_session* s, int role, void* const* followers, int n) {
+  if (!s) return fail(AMUSD_ERR_INVALID_INPUT, "null session");
+  if (role < 0 || role > 2) return fail(AMUSD_ERR_INVALID_INPUT, "role must be 0 (none), 1 (leader) or 2 (follower)");
+  if (role != 0 && !s->verify) return fail(AMUSD_ERR_INVALID_INPUT, "tensor-parallel roles need a verify model");
+  if (role == 1 && (n < 1 || n > kMaxTpOut || !followers))
+    return fail(AMUSD_ERR_INVALID_INPUT, "leader needs 1..7 follower inboxes");
+  for (auto& e : s->exec)  // the loops capture the role: rebuild them
+    for (auto& x : e)
+      if (x) { cudaGraphExecDestroy(x); x = nullptr; }
+  s->tp_role = role;
+  s->tp_nout = role == 1 ? n : 0;
+  for (int i = 0; i < s->tp_nout; ++i) s->tp_out[i] = (TpInbox*)followers[i];
+  return AMUSD_OK;
+}
+
 int amusd_session_destroy(amusd_session* s) {
   if (!s) return AMUSD_OK;
   for (auto& e : s->exec)
@@ -1049,7 +1194,7 @@ static int capture_body(amusd_session* s, int engine, int actor, cudaGraph_t bod
   for (amusd_model* m : {s->draft, s->verify}) {
     if (!m || !use_fw(m)) continue;
     m->fw_stages = env_int("AMUSD_FW_STAGES", fw_max_stages(m->cfg, 1));
-    m->fw_grid = num_sms();
+    m->fw_grid = model_sms(m);
     if (colo) m->fw_grid = m == s->draft ? draft_sms : num_sms() - draft_sms;
     m->fw_part_ok = colo && m == s->draft;
   }
@@ -1081,7 +1226,7 @@ static int capture_body(amusd_session* s, int engine, int actor, cudaGraph_t bod
     if (!m || !use_fw(m)) continue;
     m->fw_part_ok = false;
     m->fw_stages = env_int("AMUSD_FW_STAGES", fw_max_stages(m->cfg, 1));
-    m->fw_grid = num_sms();
+    m->fw_grid = model_sms(m);
   }
   if (r) return r;
   CUDA_TRY(e);

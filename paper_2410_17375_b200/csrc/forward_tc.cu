@@ -93,6 +93,28 @@ AMUSD_DEV void red_add_relaxed(int* p, int v) {
   asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// System scope (tensor-parallel peers write these words over NVLink).
+AMUSD_DEV int ld_acquire_sys(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+AMUSD_DEV void red_add_sys(int* p, int v) {
+  asm volatile("red.relaxed.sys.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+AMUSD_DEV void red_add_u64_sys(unsigned long long* p, long long v) {
+  asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+AMUSD_DEV void wait_count_sys(const int* p, int target) {
+  if (ld_acquire_sys(p) >= target) return;
+  const long long t0 = globaltimer();
+  for (;;) {
+    __nanosleep(a_poll_ns);
+    if (ld_acquire_sys(p) >= target) return;
+    if (globaltimer() - t0 > kWaitNs) __trap();
+  }
+}
+
 AMUSD_DEV void wait_count(const int* p, int target) {
   if (ld_acquire_gpu(p) >= target) return;
   const long long t0 = globaltimer();
@@ -327,13 +349,13 @@ AMUSD_DEV void tile_epilogue(const FwArgs& a, const GemmKind& ph, const __nv_bfl
       }
     }
   } else {  // LM head: per-row argmax over the tile, merged by atomicMax (order independent)
-    const int n = t * BM + nl;
-    const bool valid_n = n < ph.N && !(a.exclude_eos && n == a.eos);
+    const int n = t * BM + nl, ng = a.vocab_off + n;  // ng: global vocab id (tensor-parallel shard offset)
+    const bool valid_n = n < ph.N && !(a.exclude_eos && ng == a.eos);
 #pragma unroll
     for (int r = 0; r < BN; ++r) {
       if (r < rows) {  // live rows only (uniform)
         if (a.logits && n < ph.N) a.logits[(size_t)r * ph.N + n] = v[r] * inv[r];
-        unsigned long long key = valid_n ? argmax_key(v[r] * inv[r], n) : 0ull;
+        unsigned long long key = valid_n ? argmax_key(v[r] * inv[r], ng) : 0ull;
         key = warp_max_u64(key);
         if (lane == 0) et->kx[q * BN + r] = key;
       }
@@ -342,7 +364,11 @@ AMUSD_DEV void tile_epilogue(const FwArgs& a, const GemmKind& ph, const __nv_bfl
     if (q == 0 && lane < BN && lane < rows) {
       unsigned long long b = et->kx[lane];
       for (int w = 1; w < 4; ++w) b = et->kx[w * BN + lane] > b ? et->kx[w * BN + lane] : b;
-      atomicMax(a.best + lane, b);
+      if (a.tp > 1) {  // every rank's keys (order-independent max: the all-rank argmax everywhere)
+        for (int p = 0; p < a.tp; ++p) atomicMax_system(a.peer_best[p] + lane, b);
+      } else {
+        atomicMax(a.best + lane, b);
+      }
     }
   }
 }
@@ -1164,25 +1190,37 @@ __global__ void __launch_bounds__(kThreads, MINB)
         const int cj = j / g.ntiles, t = j - cj * g.ntiles;
         bool final = true;
         float acc[BN];
-        if (nchunks > 1) {
+        if (nchunks > 1 || g.xr) {
           // Split-K in exact int64 fixed point (2^-32): the red.adds commute, so the merged
           // tile is bit-identical whatever the chunks' arrival order (deterministic, batch
           // invariant) and no partial ever needs a merge round trip.  Layout [tile][row][128].
-          unsigned long long* acc64 = (unsigned long long*)a.ws + g.ws_off + (size_t)t * BN * BM + nl;
+          const size_t off = (size_t)g.ws_off + (size_t)t * BN * BM + nl;
+          unsigned long long* acc64 = (unsigned long long*)a.ws + off;
           // live rows only: dead rows' accumulators are never added, read or re-armed
 #pragma unroll
           for (int r = 0; r < BN; ++r) {
             if (r < L.rows) {
               const long long fx = __float2ll_rn(v[r] * 4294967296.0f);
-              asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(acc64 + r * BM), "l"(fx) : "memory");
+              if (g.xr) {  // tensor parallel: into every rank's accumulator (the fused allreduce)
+                for (int pr = 0; pr < a.tp; ++pr) red_add_u64_sys(a.peer_ws[pr] + off + r * BM, fx);
+              } else {
+                asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(acc64 + r * BM), "l"(fx) : "memory");
+              }
             }
           }
           named_bar(1, 128);
           // The tile's last chunk (grabbed after its other chunks) merges; the others publish
           // with a fire-and-forget release and move on -- no round trip in their epilogue.
+          // Tensor parallel: every chunk (mergers included) bumps every rank's tile count after
+          // a system-scope fence; each rank's local last chunk merges once all ranks' chunks
+          // have arrived.
           final = cj == nchunks - 1;
+          if (g.xr && tid == 0) {
+            __threadfence_system();
+            for (int pr = 0; pr < a.tp; ++pr) red_add_sys(a.peer_cnt[pr] + g.cnt_off + t * kPad, 1);
+          }
           if (!final) {
-            if (tid == 0) {
+            if (tid == 0 && !g.xr) {
               if (a.debug & 32) red_add_relaxed(a.tile_cnt + g.cnt_off + t * kPad, 1);  // timing experiment only
               else red_add_release(a.tile_cnt + g.cnt_off + t * kPad, 1);
             }
@@ -1195,7 +1233,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
               cp_async_wait_all();  // (lands while tid 0 awaits the count; others wait at the barrier)
             }
             if (tid == 0) {
-              wait_count(a.tile_cnt + g.cnt_off + t * kPad, nchunks - 1);
+              if (g.xr) wait_count_sys(a.tile_cnt + g.cnt_off + t * kPad, g.nchunks_total);
+              else wait_count(a.tile_cnt + g.cnt_off + t * kPad, nchunks - 1);
               a.tile_cnt[g.cnt_off + t * kPad] = 0;  // re-arm for the next phase / launch
               if (a.dbg) dbg_mark(a, phase_first(a, L, p) + j, 6, globaltimer());
             }
@@ -1268,8 +1307,16 @@ __global__ void __launch_bounds__(kThreads, MINB)
       if (tid == 0) {
         if (a.dbg) dbg_mark(a, phase_first(a, L, p) + j, 5, globaltimer());
         if (lm_last_check) {
+          if (a.tp > 1) {  // this item's keys reached every rank: count it everywhere
+            __threadfence_system();
+            for (int pr = 0; pr < a.tp; ++pr) red_add_sys(lm_counter(a.peer_sched[pr]), 1);
+          }
           const int old = atom_add_acq_rel(done + p * kPad, 1);
           if (old == a.g[kGLm].nitems - 1) {  // last LM-head item: final argmax per row
+            if (a.tp > 1) {  // ... once every rank's LM items have merged their keys here
+              wait_count_sys(lm_counter(a.sched), a.lm_items_total);
+              *lm_counter(a.sched) = 0;
+            }
             for (int r = 0; r < L.rows; ++r) {
               const unsigned long long k = atomicExch(a.best + r, 0ull);
               a.ctl->preds[r] = argmax_key_index(k);
@@ -1384,9 +1431,22 @@ static int kind_units(const char* name, int dflt) {
   return (e && *e) ? atoi(e) : dflt;
 }
 
-void build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_floats, int* cnt_ints, int* max_tiles,
+bool build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_floats, int* cnt_ints, int* max_tiles,
                  int grid) {
   const int ncols = (m.H + 2 * m.KV) * m.hd, hh = m.H * m.hd;
+  // Tensor-parallel shard: the unsharded model's chunking (dry run of the full view)
+  int kc_full[kNumGemm] = {0, 0, 0, 0, 0}, kb_full[kNumGemm] = {0, 0, 0, 0, 0};
+  if (m.tp > 1) {
+    ModelView f = m;
+    f.tp = 0; f.H = m.H_full; f.KV = m.KV_full; f.ffn = m.ffn_full;
+    FwArgs fa{};
+    size_t w0;
+    int c0, t0;
+    build_kinds(f, units_per_item, &fa, &w0, &c0, &t0, 0);
+    for (int k = 0; k < kNumGemm; ++k) { kc_full[k] = fa.g[k].kc; kb_full[k] = fa.g[k].kb; }
+  }
+  bool ok = true;
+  int gk_next = 0;  // GEMM kind index of the next kind() call (construction order below)
   const long long b_qkv = (long long)ncols * m.d * 2, b_o = (long long)m.d * hh * 2, b_gu = 2ll * m.ffn * m.d * 2;
   long long ws = 0;  // int64 elements
   int cnt = 0, mt = 0;
@@ -1418,17 +1478,28 @@ void build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_f
       const int kc2 = pick_kc(g.kb, 2 * want);
       if (kc2 > g.kc && ntiles * (g.kb / kc2) >= grid) g.kc = kc2;
     }
+    const int gk = gk_next++;
+    if (m.tp > 1) {  // the unsharded chunking; O / down reduce across the ranks
+      g.kc = kc_full[gk];
+      if (g.kb % g.kc) ok = false;
+      g.xr = gk == kGO || gk == kGDown;
+    }
     g.nchunks = g.kb / g.kc;
     g.nitems = ntiles * g.nchunks;
+    g.nchunks_total = g.xr ? kb_full[gk] / g.kc : g.nchunks;
     g.N = N; g.ldo = ldo; g.wt = wt; g.wt_stride = stride;
-    // every kind owns its accumulators / counters: consecutive phases overlap under the
-    // fine-grained dependencies
-    g.ws_off = ws;
-    g.cnt_off = cnt;
-    if (g.nchunks > 1) ws += (long long)ntiles * BM * BN;
-    cnt += ntiles * kCounterInts;
     if (epi != kEpArgmax) mt = std::max(mt, ntiles);
     return g;
+  };
+  // every kind owns its accumulators / counters (consecutive phases overlap under the
+  // fine-grained dependencies).  O and down first: their tile counts (d / 128) are the same on
+  // every tensor-parallel rank, so their regions sit at the same offsets in every rank's
+  // workspace -- the peers' red.adds target them.
+  auto place_ws = [&](GemmKind& g) {
+    g.ws_off = ws;
+    g.cnt_off = cnt;
+    if (g.nchunks > 1 || g.xr) ws += (long long)g.ntiles * BM * BN;
+    cnt += g.ntiles * kCounterInts;
   };
   const uint8_t* w0 = m.wt_layer0;
   a->g[kGQkv] = kind(kEpStoreScaled, 0, ncols / BM, m.d, ncols, ncols, w0, m.wt_layer_bytes, "QKV");
@@ -1446,6 +1517,7 @@ void build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_f
   a->g[kGDown].gnext = m.norms + 2 * m.d;   // attention RMSNorm of layer l+1 at 2l+2 (final norm at 2L)
   a->g[kGDown].gnext_stride = 2 * m.d;
   a->g[kGLm] = kind(kEpArgmax, 0, m.vocab / BM, m.d, m.vocab, m.vocab, m.wt_lm, 0, "LM");
+  for (int k : {kGO, kGDown, kGQkv, kGGu, kGLm}) place_ws(a->g[k]);
   a->g[kGLm].ssp_in = m.ssp;
   a->L = m.L;
   a->attn_max = attn_items_max(m.KV, m.S);
@@ -1454,6 +1526,7 @@ void build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_f
   *ws_floats = (size_t)std::max(ws, 1ll) * 2;
   *cnt_ints = std::max(cnt, 1);
   *max_tiles = mt;
+  return ok;
 }
 
 template <int HD, int G>

@@ -38,7 +38,15 @@ struct GemmKind {
   int epi, map;                 // epilogue, X map (0 xa, 1 attn, 2 act, 3 xb)
   int ntiles, kb, kc, nchunks, nitems;  // 128-row tiles, 64-wide K units per tile, units per item, items per tile
   int N, ldo;
+  // Tensor parallelism (row-parallel O / down): this rank holds a K slice; every chunk red.adds
+  // its int64 partial into EVERY rank's accumulator (peer memory) and bumps every rank's tile
+  // count, so each rank's merger reads the exact all-rank sum -- the allreduce fused into the
+  // split-K merge, bit-identical to the unsharded forward's sum over the same chunks.
+  int xr;                       // 1: cross-rank reduce over FwArgs::peer_*
+  int nchunks_total;            // chunks per tile over all ranks (== nchunks when xr == 0)
 };
+
+constexpr int kMaxTp = 8;       // tensor-parallel ranks of one verify model
 
 struct FwArgs {
   GemmKind g[kNumGemm];
@@ -88,6 +96,16 @@ struct FwArgs {
   const int* ab_done;
   long long* dbg;               // optional per-item timeline [item][8] (perf analysis), null in production
   int dbg_items;
+  // Tensor parallelism (tp > 1): this rank's LM-head rows are global vocab ids
+  // [vocab_off, vocab_off + N); the argmax keys go to every rank's `best` and the LM items of all
+  // ranks are counted in every rank's lm counter (sched line 2, int 4) before a rank finalizes.
+  int tp;
+  int vocab_off;
+  int lm_items_total;           // LM-head items over all ranks
+  unsigned long long* peer_ws[kMaxTp];    // every rank's split-K accumulators (self included), rank order
+  int* peer_cnt[kMaxTp];                  // every rank's split-K tile counters
+  unsigned long long* peer_best[kMaxTp];  // every rank's argmax keys
+  int* peer_sched[kMaxTp];                // every rank's schedule block (its LM arrival counter: lm_counter)
 };
 
 __host__ __device__ inline int num_phases(int L) { return 2 + 5 * L; }
@@ -100,6 +118,10 @@ int max_positions();     // longest context (max_seq) the persistent forward's s
 // [qkv | o | gate-up | down], LM head after the last layer).
 struct ModelView {
   int d, H, KV, hd, ffn, vocab, L, S;
+  // tensor parallelism: the unsharded model's heads / kv heads / ffn (0 = not sharded); the
+  // shard's kinds take the unsharded model's chunking so that every chunk partial -- and hence
+  // the int64 all-rank sum -- is the unsharded forward's
+  int tp, H_full, KV_full, ffn_full;
   const uint8_t* wt_layer0;     // tiled weights of layer 0 (qkv first)
   long long wt_layer_bytes;
   const uint8_t* wt_lm;
@@ -116,7 +138,9 @@ struct ModelView {
 // max_tiles: largest producer tile count (flag region size).
 // grid > 0: kinds for a launch on `grid` (< all) SMs (larger items, see forward_tc.cu); the
 // accumulator / counter needs never exceed the grid = 0 build's.
-void build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_floats, int* cnt_ints, int* max_tiles,
+// Returns false when a tensor-parallel shard cannot take the unsharded chunking (a rank's K slice
+// is not a whole number of chunks).
+bool build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_floats, int* cnt_ints, int* max_tiles,
                  int grid = 0);
 
 cudaError_t launch_forward(const FwArgs& a, const CUtensorMap& m_xa, const CUtensorMap& m_attn,
@@ -128,6 +152,8 @@ cudaError_t launch_cut_cleanup(int* sched, const StepCtl* ctl, float* ws, size_t
                                cudaStream_t st);
 // Draft cuts counted by the cleanup (sched line 2, int 2).
 inline int* cut_counter(int* sched) { return sched + 2 * kCounterInts + 2; }
+// LM-head items of all tensor-parallel ranks that reached this rank (sched line 2, int 4).
+__host__ __device__ inline int* lm_counter(int* sched) { return sched + 2 * kCounterInts + 4; }
 // schedule counters: grab, exit, epoch (+ cut flag), then one per phase (kCounterInts each)
 inline size_t sched_ints(int L) { return (size_t)(3 + num_phases(L)) * kCounterInts; }
 int forward_smem_bytes(int stages, int hd, int group);

@@ -72,6 +72,20 @@ struct StepCtl {
   int preds[KMAX];     // model predictions per row
 };
 
+// Tensor-parallel verify group (BASELINE config 4): the leader rank's
+// k_verify_begin snapshots the draft window once and pushes the step control
+// into every follower rank's inbox (peer HBM, payload then st.release.sys of
+// seq); followers run the same sharded forward and k_verify_end on identical
+// inputs, so every rank reaches the same predictions and the same sequence
+// state without further messages.
+struct alignas(128) TpInbox {
+  int seq;    // the leader's verify iteration this payload belongs to
+  int stop;   // 1: the leader ended its loop in k_verify_begin (error / timeout)
+  int pad[30];
+  StepCtl ctl;
+};
+constexpr int kMaxTpOut = 7;
+
 struct TraceDev {
   amusd_trace_event* ev;
   int* count;
@@ -106,6 +120,9 @@ struct ProtoArgs {
   unsigned long long jitter_seed;
   cudaGraphConditionalHandle cond;
   int has_cond;
+  TpInbox* tp_out[kMaxTpOut];  // leader: the followers' inboxes
+  int tp_nout;
+  TpInbox* tp_in;              // follower: this rank's inbox (null otherwise)
 };
 
 }  // namespace amusd

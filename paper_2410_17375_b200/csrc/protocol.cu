@@ -164,6 +164,45 @@ __global__ void k_draft_end(ProtoArgs a) {
 // ----------------------------------------------------------------- verify
 // Wait for a non-empty window outside a rollback handshake, then snapshot
 // (p_v, p_d] once (read_draft_window, coordination.py:217-228).
+// Tensor-parallel leader: push this step's control (or the stop) to every follower.
+AMUSD_DEV void tp_push(const ProtoArgs& a, const StepCtl* c, int seq, int stop) {
+  for (int i = 0; i < a.tp_nout; ++i) {
+    TpInbox* o = a.tp_out[i];
+    o->stop = stop;
+    if (!stop) {
+      o->ctl.npend = c->npend; o->ctl.m = c->m; o->ctl.rows = c->rows; o->ctl.pos0 = c->pos0;
+      for (int j = 0; j < KMAX; ++j) { o->ctl.tok[j] = c->tok[j]; o->ctl.cand[j] = c->cand[j]; }
+    }
+    st_release(&o->seq, seq);
+  }
+}
+
+// Tensor-parallel follower: the leader's snapshot of this step (same iteration count).
+AMUSD_DEV void tp_follow(const ProtoArgs& a, StepCtl* c, MailboxHdr* L) {
+  L->vb.iters += 1;
+  const int want = L->vb.iters;
+  const TpInbox* in = a.tp_in;
+  const long long t_enter = globaltimer();
+  while (ld_acquire(&in->seq) < want) {
+    if (globaltimer() - t_enter > kSpinTimeoutNs) {
+      L->vb.error = kErrTimeout;
+      L->vb.complete = 1;
+      stop_loop(a, c);
+      return;
+    }
+    __nanosleep(64);
+  }
+  if (ld_volatile(&in->stop)) {
+    L->vb.complete = 1;
+    stop_loop(a, c);
+    return;
+  }
+  c->npend = in->ctl.npend; c->m = in->ctl.m; c->rows = in->ctl.rows; c->pos0 = in->ctl.pos0;
+  for (int j = 0; j < KMAX; ++j) { c->tok[j] = in->ctl.tok[j]; c->cand[j] = in->ctl.cand[j]; }
+  c->t0 = globaltimer();
+  c->active = 1;
+}
+
 __global__ void k_verify_begin(ProtoArgs a) {
   if (threadIdx.x != 0) return;
   StepCtl* c = a.vctl;
@@ -171,6 +210,10 @@ __global__ void k_verify_begin(ProtoArgs a) {
   MailboxHdr* L = a.mb_local;
   MailboxHdr* R = a.mb_peer;
   c->active = 0;
+  if (a.tp_in) {
+    tp_follow(a, c, L);
+    return;
+  }
   R->vb.iters += 1;
   if (L != R) L->vb.iters = R->vb.iters;
   jitter(a, 0x5E, *a.vtrace.count);
@@ -180,6 +223,7 @@ __global__ void k_verify_begin(ProtoArgs a) {
     if (ld_volatile(&L->db.error)) {  // draft-side violation: end the run
       mb_write_both(&R->vb.error, &L->vb.error, ld_volatile(&L->db.error));
       mb_write_both(&R->vb.complete, &L->vb.complete, 1);
+      tp_push(a, c, L->vb.iters, 1);
       stop_loop(a, c);
       return;
     }
@@ -190,6 +234,7 @@ __global__ void k_verify_begin(ProtoArgs a) {
     if (globaltimer() - t_enter > kSpinTimeoutNs) {
       mb_write_both(&R->vb.error, &L->vb.error, kErrTimeout);
       mb_write_both(&R->vb.complete, &L->vb.complete, 1);
+      tp_push(a, c, L->vb.iters, 1);
       stop_loop(a, c);
       return;
     }
@@ -207,6 +252,7 @@ __global__ void k_verify_begin(ProtoArgs a) {
   c->pos0 = s->kv_len;
   c->t0 = globaltimer();
   c->active = 1;
+  tp_push(a, c, L->vb.iters, 0);
 }
 
 // K1 epilogue: accept the matched prefix + correction, publish to V, raise
@@ -426,6 +472,7 @@ __global__ void k_session_reset(ProtoArgs a, const int* prompt, unsigned long lo
   if (a.vctl) { a.vctl->rb_ack_local = 0; a.vctl->active = 0; a.vctl->t0 = globaltimer(); }
   if (a.dtrace.count) *a.dtrace.count = 0;
   if (a.vtrace.count) *a.vtrace.count = 0;
+  if (a.tp_in) { a.tp_in->seq = 0; a.tp_in->stop = 0; }
   if (a.coin.hash) {
     a.coin.hash[0] = mix64(coin_seed);
     a.coin.onpath[0] = 1;

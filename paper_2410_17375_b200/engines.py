@@ -129,8 +129,12 @@ class DeviceSession:
 
     def __init__(self, draft, verify, prompt_len: int, config: DecodeConfig, *, max_window: int = L.KMAX,
                  canon: torch.Tensor | None = None, trace_cap: int | None = None, jitter_ns: int = 0,
-                 jitter_seed: int = 0, mb_peer: int | None = None, mb_local: torch.Tensor | None = None):
+                 jitter_seed: int = 0, mb_peer: int | None = None, mb_local: torch.Tensor | None = None,
+                 stream_pair: tuple | None = None):
         self.lib = L.load()
+        # (verify, draft) streams; default the device's shared pair.  Ranks of a tensor-parallel
+        # group emulated on one GPU need their own: their forwards wait on each other.
+        self._stream_pair = stream_pair
         # weak: a cached session must not keep its models (GBs of HBM) alive (see _session)
         self._draft = weakref.ref(draft) if draft is not None else None
         self._verify = weakref.ref(verify) if verify is not None else None
@@ -188,9 +192,12 @@ class DeviceSession:
         L.check(self.lib.amusd_session_kernels_per_step(self._h, engine, C.byref(d), C.byref(v)))
         return d.value, v.value
 
+    def streams(self) -> tuple:
+        return self._stream_pair or streams(self.device)
+
     def prepare(self, prompt: Sequence[int]) -> None:
         """init_state(prompt) on the models (GPU prefill) and reset the mailbox."""
-        vs, ds = streams(self.device)
+        vs, ds = self.streams()
         with torch.cuda.device(self.device), torch.cuda.stream(vs):
             for m in (self.draft, self.verify):
                 if m is not None and _model_of(m)._fresh != tuple(prompt):
@@ -199,7 +206,7 @@ class DeviceSession:
 
     def launch(self, engine: int) -> tuple:
         """Enqueue the engine's graph(s); returns (start_event, end_event) on the verify stream."""
-        vs, ds = streams(self.device)
+        vs, ds = self.streams()
         with torch.cuda.device(self.device):
             start, end, dend = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             start.record(vs)
@@ -214,7 +221,7 @@ class DeviceSession:
         return start, end
 
     def collect(self, start=None, end=None) -> RunOutput:
-        vs, _ = streams(self.device)
+        vs, _ = self.streams()
         with torch.cuda.device(self.device):
             vs.synchronize()
             ms = start.elapsed_time(end) if start is not None else 0.0

@@ -156,6 +156,12 @@ class CudaModel:
     def handle(self):
         return self._h
 
+    def set_max_grid(self, sms: int) -> None:
+        """Cap the persistent forward's grid at `sms` CTAs (0 = all SMs): models sharing one GPU
+        whose forwards wait on each other (tensor-parallel ranks, co-located drafts) must be
+        co-resident."""
+        L.check(self._lib.amusd_model_set_max_grid(self._h, int(sms)))
+
     def kernels_per_forward(self) -> int:
         raise NotImplementedError
 
@@ -334,6 +340,21 @@ def weight_shape(cfg: TransformerConfig, name: str) -> tuple:
     }[leaf]
 
 
+def synthetic_weight(config: TransformerConfig, i: int, name: str, tdt, seed: int, std: float, device):
+    """Weight `name` (index i of weight_names) of the seeded synthetic model, filled on the GPU:
+    uniform with the given std from a splitmix64 counter stream (amusd_fill_uniform), norms = 1."""
+    t = torch.empty(weight_shape(config, name), dtype=tdt, device=device)
+    if name.endswith("norm"):
+        t.fill_(1.0)
+    else:
+        sub = (seed * 0x9E3779B97F4A7C15 + (i + 1) * 0xD1B54A32D192ED03) & ((1 << 64) - 1)
+        dt = L.BF16 if tdt == torch.bfloat16 else L.F32
+        with torch.cuda.device(device):
+            L.check(L.load().amusd_fill_uniform(C.c_void_p(t.data_ptr()), dt, t.numel(), sub,
+                                                std * math.sqrt(3.0), device_stream(device)))
+    return t
+
+
 class TransformerModel(CudaModel):
     """Llama-style decoder whose forwards are libamusd CUDA kernels."""
 
@@ -399,16 +420,7 @@ class TransformerModel(CudaModel):
         self.row_major = False
         torch.cuda.empty_cache()
     def _synthetic_one(self, i: int, n: str, tdt, seed: int, std: float):
-        t = torch.empty(weight_shape(self.config, n), dtype=tdt, device=self.device)
-        if n.endswith("norm"):
-            t.fill_(1.0)
-        else:
-            sub = (seed * 0x9E3779B97F4A7C15 + (i + 1) * 0xD1B54A32D192ED03) & ((1 << 64) - 1)
-            dt = L.BF16 if tdt == torch.bfloat16 else L.F32
-            with torch.cuda.device(self.device):
-                L.check(self._lib.amusd_fill_uniform(C.c_void_p(t.data_ptr()), dt, t.numel(), sub,
-                                                     std * math.sqrt(3.0), device_stream(self.device)))
-        return t
+        return synthetic_weight(self.config, i, n, tdt, seed, std, self.device)
 
     def _synthetic(self, tdt, seed: int, std: float) -> dict:
         """Deterministic random init on the GPU: uniform with the given std, norms = 1."""
