@@ -54,9 +54,10 @@ def parse():
     ap.add_argument("--profile-only", action="store_true", help="one AMUSD decode, no extras (for ncu)")
     ap.add_argument("--engines", default="ar,sync,amusd", help="subset of ar,sync,amusd to time")
     ap.add_argument("--no-extras", action="store_true", help="skip roofline/e2e/cpu legs (quick sweeps)")
-    ap.add_argument("--layout", default="auto", choices=["auto", "replicas", "split"],
+    ap.add_argument("--layout", default="auto", choices=["auto", "replicas", "split", "pairs"],
                     help="N>1: auto = the paper's split pair at N=2 (draft on rank 0's GPU, verify on rank 1's: "
-                         "BASELINE config 2) and independent co-located pairs per GPU otherwise (replicas)")
+                         "BASELINE config 2) and independent co-located pairs per GPU otherwise (replicas); "
+                         "pairs = N/2 independent split pairs (BASELINE config 5 with --prompt-len 4096)")
     return ap.parse_args()
 
 
@@ -114,47 +115,64 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-# ------------------------------------------------------- split pair (config 2)
+# ------------------------------------------------- split pairs (configs 2 and 5)
 def split_arm(args, rank: int, world: int, local_rank: int):
-    """BASELINE config 2 (the paper's deployment): draft on GPU0 (rank 0), verify on GPU1 (rank 1),
-    mailbox copies in each GPU's HBM written by their single writers over NVLink P2P.
+    """BASELINE config 2 (the paper's deployment, N=2) and config 5 (N/2 independent pairs,
+    --layout pairs, long prompts via --prompt-len): in every pair the draft sits on one GPU
+    (even rank) and the verify on the next (odd rank); the mailbox copies live in each GPU's HBM
+    and are written by their single writers over NVLink P2P.  Pairs never communicate.
 
-    value = generated tokens / device-timed decode (max over the two GPUs); e2e = the public
-    API call (decode_speculative_async_split: host prompt in, prefill, IPC mailbox exchange,
-    host tokens and trace out), wall clock, max over ranks; roofline = each GPU's persistent
-    forward timed alone (CUDA events); the reference simulator's prediction for these latencies
-    is printed beside the measurement (section 8(f)3)."""
+    value = all pairs' generated tokens / the device-timed decode (max over every GPU); e2e = the
+    public API call (decode_speculative_async_split: host prompt in, prefill, IPC mailbox
+    exchange, host tokens and trace out), wall clock, max over ranks; prefill (TTFT's GPU part) is
+    timed separately; roofline = each GPU's persistent forward timed alone (CUDA events); the
+    reference simulator's prediction for these latencies is printed beside the measurement
+    (section 8(f)3)."""
     import torch
+    import torch.distributed as dist
     import paper_2410_17375_b200 as P
     from paper_2410_17375_b200 import _lib as L
+    from paper_2410_17375_b200 import calibrate as CB
     from paper_2410_17375_b200 import split as SP
     from paper_2410_17375_b200.split import SplitLink, decode_speculative_async_split
-    if world != 2:
-        raise SystemExit("--layout split needs exactly 2 ranks")
-    local_rank %= torch.cuda.device_count()   # 2 ranks on 1 GPU: functional check of the same path
+    if world % 2:
+        raise SystemExit("split pairs need an even number of ranks")
+    npairs = world // 2
+    local_rank %= torch.cuda.device_count()   # fewer GPUs than ranks: functional check of the same path
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    groups = [dist.new_group([2 * p, 2 * p + 1]) for p in range(npairs)]
+    link = SplitLink(group=groups[rank // 2])
     TC = P.TransformerConfig
     N, Plen = args.new_tokens, args.prompt_len
     max_seq = Plen + N + 64
-    link = SplitLink()
     if link.role == "draft":
-        base = P.TransformerModel(TC.llama_1b(max_seq=max_seq), seed=1, device=dev)
+        base = P.TransformerModel(TC.llama_1b(max_seq=max_seq), seed=1, device=dev, keep_row_major=False)
         model = P.AgreementDraft(base, args.rho, coin_seed=1234)
     else:
-        base = model = P.TransformerModel(TC.llama_8b(max_seq=max_seq), seed=0, device=dev)
+        base = model = P.TransformerModel(TC.llama_8b(max_seq=max_seq), seed=0, device=dev, keep_row_major=False)
+    if torch.cuda.device_count() < world:   # ranks share a GPU: keep their loops co-resident
+        share = max(1, world // torch.cuda.device_count())
+        base.set_max_grid(torch.cuda.get_device_properties(dev).multi_processor_count // share)
     cfg_m = base.config
     prompt = synthetic_prompt(Plen, 128256)
     cfg = P.DecodeConfig(max_new_tokens=N, draft_window_k=args.k, max_draft_lead=args.lead or None)
     for _ in range(args.warmup):
         decode_speculative_async_split(model, prompt, cfg, link=link, max_window=args.window)
-    total, toks, launches, ref_tokens = 0.0, 0, 0, None
-    link.barrier()
+    total, toks, launches, ref_tokens, prefill = 0.0, 0, 0, None, []
+    dist.barrier()
     torch.cuda.synchronize()
     cm = ClockSampler(local_rank).__enter__()
     for _ in range(args.steps):
+        # prefill timed apart (CUDA events); the decode below then starts from the fresh state
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        base.init_state(prompt)
+        e1.record()
+        e1.synchronize()
+        prefill.append(e0.elapsed_time(e1))
         res, (dms, vms) = decode_speculative_async_split(model, prompt, cfg, link=link, max_window=args.window)
-        total += max(dms, vms)      # device-timed, max over the two GPUs
+        total += max(dms, vms)      # device-timed, max over the pair's two GPUs
         toks += len(res.tokens)
         launches += SP.last_run["iters"] * SP.last_run["kernels_per_step"]   # this rank's GPU
         ref_tokens = ref_tokens or res.tokens
@@ -162,10 +180,7 @@ def split_arm(args, rank: int, world: int, local_rank: int):
             raise SystemExit("split-pair output changed between runs -- parity broken")
     torch.cuda.synchronize()
     cm.__exit__(None, None, None)
-    peer_launches = link.exchange(launches)
-    clocks = {"mine": cm.summary(), "peer": None}
-    clocks["peer"] = link.exchange(clocks["mine"])
-    # parity: the split tokens equal the verify model's own greedy (AR) path
+    # parity: the pair's tokens equal the verify model's own greedy (AR) path
     ar_ok = None
     if link.role == "verify":
         from paper_2410_17375_b200.engines import canonical_path
@@ -173,63 +188,75 @@ def split_arm(args, rank: int, world: int, local_rank: int):
     ar_ok = next(x for x in (ar_ok, link.exchange(ar_ok)) if x is not None)
     if not ar_ok:
         raise SystemExit("split-pair AMUSD output differs from the verify model's AR path -- parity broken")
-    # e2e through the public API (wall clock around the whole call), max over ranks
+    # e2e through the public API (wall clock around the whole call), max over every rank
     e2e_ms, e2e_toks = [], 0
     for _ in range(max(1, args.steps)):
-        link.barrier()
+        dist.barrier()
         t0 = time.perf_counter()
         r2, _ = decode_speculative_async_split(model, prompt, cfg, link=link, max_window=args.window)
-        dt = (time.perf_counter() - t0) * 1000.0
-        e2e_ms.append(max(dt, link.exchange(dt)))
+        e2e_ms.append((time.perf_counter() - t0) * 1000.0)
         e2e_toks += len(r2.tokens)
-    # per-GPU roofline: each GPU's persistent forward alone (1 row; draft step / verify window of 1)
-    from paper_2410_17375_b200 import calibrate as CB
+    # per-GPU roofline: each GPU's persistent forward alone (1 row) at the prompt's context
     base.init_state(prompt)
     fms = CB.forward_ms(base, 1, iters=20)
     fbytes = cfg_m.step_weight_bytes() + cfg_m.kv_bytes_per_token() * (Plen + 1)
-    vrows = None
-    if link.role == "verify":
-        vrows = {m: CB.forward_ms(base, m) for m in (1, 2, 4, 8, 16)}
-    mine_f = {"role": link.role, "ms": fms, "bytes": fbytes, "vrows": vrows}
-    peer_f = link.exchange(mine_f)
-    fw = {x["role"]: x for x in (mine_f, peer_f)}
+    vrows = {m: CB.forward_ms(base, m) for m in (1, 2, 4, 8, 16)} if link.role == "verify" else None
+    mine = {"rank": rank, "role": link.role, "ms": fms, "bytes": fbytes, "vrows": vrows, "toks": toks,
+            "total": total, "prefill": max(prefill), "e2e_ms": sum(e2e_ms), "e2e_toks": e2e_toks,
+            "launches": launches, "clocks": cm.summary(), "verify_steps": res.stats.verify_steps,
+            "rollbacks": res.stats.rollbacks, "drafted": res.stats.drafted_tokens}
+    allr = [None] * world
+    dist.all_gather_object(allr, mine)
+    if rank != 0:
+        return
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    gbs = {k: v["bytes"] / v["ms"] / 1e6 for k, v in fw.items()}
+    verify_ranks = [r for r in allr if r["role"] == "verify"]
+    draft_ranks = [r for r in allr if r["role"] == "draft"]
+    tok_all = sum(r["toks"] for r in verify_ranks)
+    t_max = max(r["total"] for r in allr)
+    v = tok_all / (t_max / 1000.0)
+    gbs = {r["role"] + str(r["rank"] // 2): r["bytes"] / r["ms"] / 1e6 for r in allr}
+    vr0 = verify_ranks[0]
     calib = None
     try:
-        vb, vp = CB.fit_linear(fw["verify"]["vrows"])
-        lat = CB.Latencies(0.0, fw["draft"]["ms"], vb, vp, Plen)
+        vb, vp = CB.fit_linear(vr0["vrows"])
+        lat = CB.Latencies(0.0, draft_ranks[0]["ms"], vb, vp, Plen)
         calib = {"latency_ms": {"draft_per_token_ms": round(lat.draft_per_token_ms, 5),
                                 "verify_base_ms": round(vb, 5), "verify_per_token_ms": round(vp, 5)},
-                 "predicted_tokens_per_s": {f"rho{r}": CB.predict(lat, r, n_tokens=N) for r in (args.rho, 0.9)}}
+                 "predicted_tokens_per_s_per_pair": {f"rho{r}": CB.predict(lat, r, n_tokens=N) for r in (args.rho, 0.9)}}
     except Exception as exc:
         calib = {"unavailable": f"{type(exc).__name__}: {exc}"}
-    if rank == 0:
-        v = toks / (total / 1000.0)
-        print(json.dumps({
-            "metric": METRIC, "value": round(v, 2), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(total / args.steps, 3), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (random-init weights, seeded prompt)",
-            "config": {"workload": "cfg2: Llama-3.2-1B-shaped draft on GPU0 + Llama-3.1-8B-shaped verify on GPU1, "
-                                   "P2P mailbox over NVLink", "rho": args.rho, "new_tokens": N, "prompt_len": Plen,
-                       "parallelism": "split pair (draft | verify)", "gpus_visible": torch.cuda.device_count(),
-                       "l2": "weights (17.5 GB) >> 126 MB L2: no flush needed"},
-            "amusd": {"tokens_per_s": round(v, 3), "verify_steps": res.stats.verify_steps,
-                      "rollbacks": res.stats.rollbacks, "drafted": res.stats.drafted_tokens,
-                      "tokens_equal_ar": bool(ar_ok)},
-            "roofline": {"bound": "hbm", "kernel": "k_forward (persistent tcgen05 forward), 1 row, each GPU alone",
-                         "achieved": round(gbs["verify"], 1), "peak": hbm_peak, "unit": "GB/s",
-                         "frac": round(gbs["verify"] / hbm_peak, 4), "traffic": None,
-                         "per_gpu": {k: {"ms": round(fw[k]["ms"], 4), "GB/s": round(gbs[k], 1),
-                                         "frac": round(gbs[k] / hbm_peak, 4)} for k in fw}},
-            "calibration": calib,
-            "cpu_baseline": None,
-            "e2e": {"value": round(e2e_toks / (sum(e2e_ms) / 1000.0), 2), "unit": "tokens/s",
-                    "h2d_bytes_per_step": 4 * Plen * 2, "d2h_bytes_per_step": 4 * (N + L.KMAX),
-                    "includes": "prefill on both GPUs + IPC mailbox exchange + both loops + token/trace read-back"},
-            "gpu_launches": int(launches + peer_launches), "clocks": clocks}))
+    e2e_t = max(r["e2e_ms"] for r in allr)
+    workload = ("cfg2: Llama-3.2-1B-shaped draft on GPU0 + Llama-3.1-8B-shaped verify on GPU1, P2P mailbox over "
+                "NVLink" if npairs == 1 else
+                f"cfg5: {npairs} independent split pairs (1B-shaped draft GPU | 8B-shaped verify GPU) on {world} GPUs")
+    print(json.dumps({
+        "metric": METRIC, "value": round(v, 2), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 3), "higher_is_better": True,
+        "scaling": "strong" if npairs == 1 else "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init weights, seeded prompt)",
+        "config": {"workload": workload, "rho": args.rho, "new_tokens": N, "prompt_len": Plen,
+                   "parallelism": f"{npairs} split pair(s) (draft | verify)", "gpus_visible": torch.cuda.device_count(),
+                   "l2": "weights (17.5 GB) >> 126 MB L2: no flush needed"},
+        "amusd": {"tokens_per_s": round(v, 3), "tokens_per_s_per_pair": round(v / npairs, 3),
+                  "verify_steps": vr0["verify_steps"], "rollbacks": vr0["rollbacks"], "drafted": vr0["drafted"],
+                  "tokens_equal_ar": bool(ar_ok)},
+        "prefill_ms": {"max_over_gpus": round(max(r["prefill"] for r in allr), 3),
+                       "draft": round(max(r["prefill"] for r in draft_ranks), 3),
+                       "verify": round(max(r["prefill"] for r in verify_ranks), 3),
+                       "note": f"init_state of the {Plen}-token prompt (not in value)"},
+        "roofline": {"bound": "hbm", "kernel": "k_forward (persistent tcgen05 forward), 1 row, each GPU alone",
+                     "achieved": round(vr0["bytes"] / vr0["ms"] / 1e6, 1), "peak": hbm_peak, "unit": "GB/s",
+                     "frac": round(vr0["bytes"] / vr0["ms"] / 1e6 / hbm_peak, 4), "traffic": None,
+                     "per_gpu": {k: {"GB/s": round(x, 1), "frac": round(x / hbm_peak, 4)} for k, x in gbs.items()}},
+        "calibration": calib,
+        "cpu_baseline": None,
+        "e2e": {"value": round(sum(r["e2e_toks"] for r in verify_ranks) / (e2e_t / 1000.0), 2), "unit": "tokens/s",
+                "h2d_bytes_per_step": 4 * Plen * 2 * npairs, "d2h_bytes_per_step": 4 * (N + L.KMAX) * npairs,
+                "includes": "prefill on both GPUs + IPC mailbox exchange + both loops + token/trace read-back"},
+        "gpu_launches": int(sum(r["launches"] for r in allr)),
+        "clocks": {f"rank{r['rank']}": r["clocks"] for r in allr}}))
 
 
 # --------------------------------------------------------------- GPU arm
@@ -588,13 +615,13 @@ def main():
         args.layout = "split" if world == 2 else "replicas"
     if world > 1:
         import torch
-        if args.layout != "split":
+        if args.layout not in ("split", "pairs"):
             torch.cuda.set_device(local_rank)
         # the split pair's link is object collectives only (gloo); replicas time with NCCL
-        torch.distributed.init_process_group("nccl" if args.impl == "amusd" and args.layout != "split" else "gloo")
+        torch.distributed.init_process_group("nccl" if args.impl == "amusd" and args.layout == "replicas" else "gloo")
     if args.impl == "reference":
         reference_arm(args, rank, world)
-    elif args.layout == "split":
+    elif args.layout in ("split", "pairs"):
         split_arm(args, rank, world, local_rank)
     else:
         out = gpu_arm(args, rank, world, local_rank)

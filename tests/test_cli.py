@@ -62,3 +62,41 @@ def test_compare_run_trace_on_gpu(tmp_path, capsys, kind):
     assert cli.main(["trace", str(p), "async_speculative-t0"]) == 0
     lines = capsys.readouterr().out.strip().splitlines()
     assert lines[0] == "t_ms,verified_tokens" and lines[-1].endswith(",40")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["agreement_pair", "agreement_pair_rho09_k6", "hash_chain", "scripted_eos"])
+def test_artifacts_match_reference_cli(tmp_path, case):
+    """The CUDA CLI's artifacts against the UNMODIFIED reference CLI's on the same config
+    (tests/golden/cli.json, oracle/make_cli_golden.py): tokens.json verbatim, the stats.json
+    schema, every timing-independent statistic, the trace.csv header and (AR / sync-SD) the
+    per-kind event counts."""
+    import csv
+    import io
+    from pathlib import Path
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    gold = json.loads((Path(__file__).parent / "golden" / "cli.json").read_text())
+    g = gold["cases"][case]
+    cfg = json.loads(json.dumps(g["config"]))
+    if cfg["model"].get("script_path") == "@SCRIPT":
+        (tmp_path / "script.json").write_text(json.dumps(gold["script"]))
+        cfg["model"]["script_path"] = str(tmp_path / "script.json")
+    cfg["execution"] = {"backend": "cuda", "out_dir": str(tmp_path / "out")}
+    p = tmp_path / "c.json"
+    p.write_text(json.dumps(cfg))
+    assert cli.main(["run", str(p)]) == 0
+    for strat, ref in g["runs"].items():
+        d = tmp_path / "out" / f"{strat}-t0"
+        assert json.loads((d / "tokens.json").read_text()) == ref["tokens_json"], strat
+        stats = json.loads((d / "stats.json").read_text())
+        assert sorted(stats) == ref["stats_keys"]
+        assert {k: stats[k] for k in ref["stats"]} == ref["stats"], strat
+        rows = list(csv.reader(io.StringIO((d / "trace.csv").read_text())))
+        assert rows[0] == ref["trace_header"]
+        if ref["trace_kinds"] is not None:
+            kinds = {}
+            for r in rows[1:]:
+                kinds[r[2]] = kinds.get(r[2], 0) + 1
+            assert kinds == ref["trace_kinds"], strat
