@@ -165,6 +165,13 @@ int amusd_model_release_row_major(amusd_model* m);
 /* Perf analysis only: run amusd_time_forward's persistent launches on `sms`
  * SMs (0 = all), e.g. the share a co-located session gives the model. */
 int amusd_model_set_grid(amusd_model* m, int sms);
+/* Compute-bound prompt prefill (init_state models.py:109-118):
+ * with a workspace set, init_state of a bf16 tcgen05 model caches prompts of
+ * >= 64 positions (AMUSD_PREFILL_MIN) as dense M128 N256 tcgen05 GEMMs over all
+ * prompt tokens plus a causal attention, instead of 16-row decode forwards.
+ * buf = NULL detaches it.  The caller owns the memory (the library never allocates). */
+size_t amusd_prefill_bytes(amusd_model* m, int max_tokens);
+int amusd_model_set_prefill(amusd_model* m, void* buf, size_t bytes, int max_tokens);
 /* Cap every persistent launch of the model (API forwards and non-co-located
  * engine loops) at `sms` CTAs (0 = all SMs).  Ranks of a tensor-parallel group
  * emulated on ONE GPU need this: their forwards wait on each other, so their

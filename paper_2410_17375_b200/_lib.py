@@ -86,6 +86,8 @@ SIGNATURES = [
     ("amusd_tp_connect", _I, [_VP, _P(TpPeer), _I]),
     ("amusd_model_set_max_grid", _I, [_VP, _I]),
     ("amusd_peer_enable", _I, [_I, _I]),
+    ("amusd_prefill_bytes", _SZ, [_VP, _I]),
+    ("amusd_model_set_prefill", _I, [_VP, _VP, _SZ, _I]),
     ("amusd_session_tp_inbox", _I, [_VP, _P(_VP)]),
     ("amusd_session_set_tp", _I, [_VP, _I, _P(_VP), _I]),
     ("amusd_model_set_path", _I, [_VP, _I]),

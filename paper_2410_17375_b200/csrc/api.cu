@@ -20,6 +20,7 @@
 #include "transformer.h"
 #include "gemm_tc.h"
 #include "forward_tc.h"
+#include "prefill.h"
 
 using namespace amusd;
 
@@ -130,6 +131,9 @@ struct amusd_model {
   bool row_major = true;  // row-major layer weights still valid (amusd_model_release_row_major)
   long long* fw_dbg = nullptr;  // optional per-item timeline (amusd_model_set_timeline)
   int fw_dbg_items = 0;
+  // compute-bound prompt prefill (prefill.cu), caller workspace (amusd_model_set_prefill)
+  pf::Work pf{};
+  bool pf_ready = false;
   // tensor-parallel shard (amusd_tf_create_shard): tp.tp_size == 0 when not sharded
   amusd_tp_shard tp{};
   bool tp_connected = false;
@@ -779,6 +783,27 @@ int amusd_model_release_row_major(amusd_model* m) {
   return AMUSD_OK;
 }
 
+size_t amusd_prefill_bytes(amusd_model* m, int max_tokens) {
+  if (!m || m->kind != 0 || max_tokens < 1) return 0;
+  const amusd_tf_config& c = m->cfg;
+  return pf::work_bytes(max_tokens, c.d_model, c.n_heads, c.n_kv_heads, c.head_dim, c.ffn);
+}
+
+int amusd_model_set_prefill(amusd_model* m, void* buf, size_t bytes, int max_tokens) {
+  if (!m) return fail(AMUSD_ERR_INVALID_INPUT, "null model");
+  if (!buf) { m->pf_ready = false; return AMUSD_OK; }
+  if (m->kind != 0 || !m->tc || !m->fw_ready)
+    return fail(AMUSD_ERR_UNSUPPORTED, "the prefill runs bf16 tcgen05 transformer models only");
+  if (max_tokens < 1 || bytes < amusd_prefill_bytes(m, max_tokens))
+    return fail(AMUSD_ERR_INVALID_INPUT, "prefill buffer too small");
+  const amusd_tf_config& c = m->cfg;
+  pf::carve(&m->pf, buf, max_tokens, c.d_model, c.n_heads, c.n_kv_heads, c.head_dim, c.ffn);
+  if (!pf::make_maps(&m->pf, c.d_model, c.n_heads * c.head_dim, c.ffn))
+    return fail(AMUSD_ERR_CUDA, "prefill tensor maps (cuTensorMapEncodeTiled) failed");
+  m->pf_ready = true;
+  return AMUSD_OK;
+}
+
 int amusd_model_set_max_grid(amusd_model* m, int sms) {
   if (!m || sms < 0) return fail(AMUSD_ERR_INVALID_INPUT, "bad argument");
   if (m->kind != 0) return AMUSD_OK;
@@ -848,9 +873,52 @@ static int api_forward(amusd_model* m, int pos0, const int* rows_tok, int rows, 
   return AMUSD_OK;
 }
 
+// Prompt positions [0, n) into the KV cache as dense GEMMs over all n tokens (prefill.cu):
+// the decode forward would re-stream every weight once per 16 positions.
+static int prefill_forward(amusd_model* m, int n, cudaStream_t st) {
+  const amusd_tf_config& c = m->cfg;
+  pf::Work& W = m->pf;
+  const int d = c.d_model, H = c.n_heads, KV = c.n_kv_heads, hd = c.head_dim, L = c.n_layers;
+  const int ncols = (H + 2 * KV) * hd, hh = H * hd;
+  auto gemm = [&](const CUtensorMap& mx, const uint8_t* wt, int ntiles, int K, int epi, float* out,
+                  __nv_bfloat16* out_b, int ldo) -> cudaError_t {
+    pf::GemmArgs g{};
+    g.wt = wt; g.ntiles = ntiles; g.kb = K / 64; g.M = n; g.epi = epi; g.out = out; g.out_b = out_b; g.ldo = ldo;
+    g.inv = W.inv;
+    return pf::launch_gemm(mx, g, st);
+  };
+  CUDA_TRY(pf::launch_embed(m->tok, (const __nv_bfloat16*)m->w.embed, W.h, n, d, st));
+  for (int l = 0; l < L; ++l) {
+    __nv_bfloat16* kc = (__nv_bfloat16*)m->kc + (size_t)l * m->kv_layer_elems;
+    __nv_bfloat16* vc = (__nv_bfloat16*)m->vc + (size_t)l * m->kv_layer_elems;
+    CUDA_TRY(pf::launch_norm(W.h, m->fw_norms + (size_t)(2 * l) * d, W.x, W.inv, n, d, c.norm_eps, st));
+    CUDA_TRY(gemm(W.map_x_d, m->wt_qkv[l], ncols / 128, d, pf::kEpStoreScaled, W.qkv, nullptr, ncols));
+    CUDA_TRY(pf::launch_rope_kv(W.qkv, m->w.rope_cos, m->w.rope_sin, kc, vc, n, H, KV, hd, c.max_seq, st));
+    if (l == L - 1) break;  // the last layer's K / V is all the decode steps need
+    CUDA_TRY(pf::launch_attention(W.qkv, kc, vc, W.x, n, H, KV, hd, c.max_seq, 1.0f / sqrtf((float)hd), st));
+    CUDA_TRY(gemm(W.map_x_hh, m->wt_o[l], d / 128, hh, pf::kEpResid, W.h, nullptr, d));
+    CUDA_TRY(pf::launch_norm(W.h, m->fw_norms + (size_t)(2 * l + 1) * d, W.x, W.inv, n, d, c.norm_eps, st));
+    CUDA_TRY(gemm(W.map_x_d, m->wt_gu[l], c.ffn / 64, d, pf::kEpGateUp, nullptr, W.act, c.ffn));
+    CUDA_TRY(gemm(W.map_act, m->wt_d[l], d / 128, c.ffn, pf::kEpResid, W.h, nullptr, d));
+  }
+  return AMUSD_OK;
+}
+
+static int prefill_min_tokens() {
+  static int v = -1;
+  if (v < 0) v = std::max(1, env_int("AMUSD_PREFILL_MIN", 64));
+  return v;
+}
+
 // Bring the cache up to len-1 (at most `keep` pending tokens stay uncached).
 static int catch_up(amusd_model* m, int keep, cudaStream_t st) {
   if (m->kv_len >= m->len) m->kv_len = m->len - 1;
+  const int todo = m->len - keep - m->kv_len;
+  if (m->pf_ready && m->kv_len == 0 && m->tp.tp_size < 2 && use_fw(m) && todo >= prefill_min_tokens() &&
+      todo <= m->pf.max_tokens) {
+    if (int r = prefill_forward(m, todo, st)) return r;
+    m->kv_len = todo;
+  }
   while (m->len - m->kv_len > keep) {
     const int rows = std::min(KMAX, m->len - m->kv_len - keep);
     int r = api_forward(m, m->kv_len, m->htok.data() + m->kv_len, rows, nullptr, st);

@@ -359,7 +359,7 @@ class TransformerModel(CudaModel):
     """Llama-style decoder whose forwards are libamusd CUDA kernels."""
 
     def __init__(self, config: TransformerConfig, weights: dict | None = None, seed: int = 0,
-                 device=None, init_std: float = 0.02, keep_row_major: bool = True):
+                 device=None, init_std: float = 0.02, keep_row_major: bool = True, prefill: bool = True):
         super().__init__(config.vocab_size, config.eos_token, device)
         if config.dtype not in ("bf16", "fp32"):
             raise InvalidInputError(f"dtype must be 'bf16' or 'fp32', got {config.dtype!r}")
@@ -404,8 +404,28 @@ class TransformerModel(CudaModel):
                                           C.c_void_p(self._state.data_ptr()), nbytes))
         settle(self.device)
         self.row_major = True
+        self._prefill = None
+        if prefill and config.dtype == "bf16" and config.use_tensor_cores and config.max_seq >= 128:
+            self.set_prefill(True)
         if not keep_row_major:
             self.release_row_major()
+
+    def set_prefill(self, on: bool) -> None:
+        """Attach (or detach) the compute-bound prompt prefill: init_state of
+        >= 64-position prompts runs as dense tcgen05 GEMMs over all prompt tokens plus a causal
+        attention instead of 16-row decode forwards.  Workspace ~ max_seq x (d, ffn, qkv) HBM."""
+        if not on:
+            L.check(self._lib.amusd_model_set_prefill(self._h, None, 0, 0))
+            self._prefill = None
+            return
+        n = self.config.max_seq
+        nbytes = self._lib.amusd_prefill_bytes(self._h, n)
+        if nbytes == 0:
+            raise InvalidInputError("this model has no prefill path")
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        with torch.cuda.device(self.device):
+            L.check(self._lib.amusd_model_set_prefill(self._h, C.c_void_p(buf.data_ptr()), nbytes, n))
+        self._prefill = buf
 
     def release_row_major(self) -> None:
         """Free the row-major layer weights (the persistent forward streams only its
