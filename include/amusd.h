@@ -154,10 +154,19 @@ int amusd_peer_enable(int device, int peer);
 /* Forward implementation of a bf16 tensor-core-shaped transformer (perf A/B
  * and parity tests; not in the reference, whose models are Python mocks):
  * 0 = persistent tcgen05 forward (default, one launch per forward),
- * 1 = per-kernel tcgen05 path (1 + 5L + 2 launches), 2 = SIMT GEMV path.
+ * 1 = per-kernel tcgen05 path (1 + 5L + 2 launches), 2 = SIMT GEMV path,
+ * 3 = persistent SIMT decode forward (decode_gv.cu: one launch, static
+ *     per-CTA row partitions, fused RMSNorm + GEMV over the row-major weights;
+ *     the draft model's path -- its forwards carry 1-2 rows).
  * Applies to launches enqueued afterwards (sessions capture it per engine). */
-enum { AMUSD_PATH_PERSISTENT = 0, AMUSD_PATH_KERNELS = 1, AMUSD_PATH_SIMT = 2 };
+enum { AMUSD_PATH_PERSISTENT = 0, AMUSD_PATH_KERNELS = 1, AMUSD_PATH_SIMT = 2, AMUSD_PATH_DECODE = 3 };
 int amusd_model_set_path(amusd_model* m, int path);
+/* The decode forward (AMUSD_PATH_DECODE) streams its own weight layout: 16-row x 512-K
+ * units, 16-byte chunks swizzled for ldmatrix.  amusd_decode_bytes = its size (0: shapes not
+ * supported); amusd_model_set_decode tiles the row-major weights into the caller's buffer
+ * (the library never allocates), buf = NULL detaches it. */
+size_t amusd_decode_bytes(amusd_model* m);
+int amusd_model_set_decode(amusd_model* m, void* buf, size_t bytes);
 /* Drop the caller's row-major layer weights from the model (the persistent path
  * reads only its tile-contiguous copy): afterwards the caller may free them
  * (8B: 16 GB) and only AMUSD_PATH_PERSISTENT remains selectable. */

@@ -15,6 +15,7 @@
 
 #include "../../include/amusd.h"
 #include "common.cuh"
+#include "decode_gv.h"
 #include "internal.h"
 #include "protocol.h"
 #include "transformer.h"
@@ -128,6 +129,13 @@ struct amusd_model {
   int grid_override = 0;            // amusd_model_set_grid: SMs of amusd_time_forward launches (0 = all)
   int max_grid = 0;                 // amusd_model_set_max_grid: cap of every persistent launch (0 = all SMs)
   int path = AMUSD_PATH_PERSISTENT;
+  // persistent SIMT decode forward (decode_gv.cu, AMUSD_PATH_DECODE): counters, per-CTA sums
+  // of squares, attention split partials
+  bool gv_ok = false;
+  const uint8_t* gv_wt = nullptr;  // decode-layout weights (amusd_model_set_decode, caller-owned)
+  int* gv_sync = nullptr;
+  float* gv_ss = nullptr;
+  float* gv_attn_ws = nullptr;
   bool row_major = true;  // row-major layer weights still valid (amusd_model_release_row_major)
   long long* fw_dbg = nullptr;  // optional per-item timeline (amusd_model_set_timeline)
   int fw_dbg_items = 0;
@@ -258,6 +266,14 @@ static size_t tf_carve(const amusd_tf_config* c, void* base, amusd_model* m, con
     fattn_ws = cv.take<float>((size_t)c->n_kv_heads * KMAX * fw::attn_splits(c->max_seq) * group * (c->head_dim + 2));
     fattn_cnt = cv.take<int>((size_t)c->n_kv_heads * KMAX * fw::kCounterInts);
   }
+  const bool gvok = tc && gv::supported(c->d_model, c->n_heads, c->n_kv_heads, c->head_dim, c->ffn, c->vocab);
+  int* gsync = nullptr;
+  float *gss = nullptr, *gattn = nullptr;
+  if (gvok) {
+    gsync = cv.take<int>(gv::sync_ints(c->n_kv_heads));
+    gss = cv.take<float>(gv::ss_floats());
+    gattn = cv.take<float>(gv::attn_ws_floats(c->n_kv_heads, group, c->head_dim, c->max_seq));
+  }
   if (m) {
     m->attn_ws = attn_ws; m->attn_cnt = attn_cnt;
     m->fw_sched = fsched; m->fw_best = fbest; m->fw_ws = fws; m->fw_tile_cnt = fcnt; m->fw_norms = fnorms;
@@ -270,6 +286,7 @@ static size_t tf_carve(const amusd_tf_config* c, void* base, amusd_model* m, con
       m->fw_cnt_ints = (size_t)cints;
       m->fw_attn_cnt_ints = (size_t)c->n_kv_heads * KMAX * fw::kCounterInts;
     }
+    m->gv_ok = gvok; m->gv_sync = gsync; m->gv_ss = gss; m->gv_attn_ws = gattn;
     m->fw_xb = fxb; m->fw_sspb = fsspb; m->fw_tflag = ftflag; m->fw_agrp = fagrp;
     m->tc = tc; m->xa_b = xa_b; m->attn_b = attn_b; m->act_b = act_b; m->inv = inv; m->ssp = ssp_b; m->tc_ws = ws; m->tc_cnt = cnt; m->tiled = tiled;
     m->seq = seq; m->tok = tok; m->api_ctl = ctl; m->kc = kc; m->vc = vc; m->h = h; m->qkv = qkv;
@@ -417,6 +434,12 @@ static int tc_kernel(amusd_model* m, StepCtl* ctl, int l, int which, cudaStream_
 static bool use_fw(const amusd_model* m) {
   return m->kind == 0 && m->tc && m->fw_ready && fw_enabled() && m->path == AMUSD_PATH_PERSISTENT;
 }
+// Persistent SIMT decode forward (decode_gv.cu): the draft's path (AMUSD_PATH_DECODE).
+static bool use_gv(const amusd_model* m) {
+  return m->kind == 0 && m->gv_ok && m->gv_wt && m->path == AMUSD_PATH_DECODE;
+}
+// A persistent forward (tcgen05 work queue or SIMT decode): one launch, grid from fw_grid.
+static bool use_persistent(const amusd_model* m) { return use_fw(m) || use_gv(m); }
 // Per-kernel tcgen05 path for 16-row forwards (2-row draft steps take the SIMT GEMVs).
 static bool use_tc(const amusd_model* m, int nr) {
   return m->kind == 0 && m->tc && nr > 2 && m->path != AMUSD_PATH_SIMT;
@@ -464,6 +487,38 @@ static int fw_forward(amusd_model* m, StepCtl* ctl, cudaStream_t st, bool want_l
   return AMUSD_OK;
 }
 
+// The whole forward as one persistent SIMT launch (decode_gv.cu).
+static int gv_forward(amusd_model* m, StepCtl* ctl, cudaStream_t st, bool want_logits) {
+  const amusd_tf_config& c = m->cfg;
+  gv::GvArgs a;
+  std::memset(&a, 0, sizeof(a));
+  const gv::Layout t = gv::layout(c.d_model, c.n_heads, c.n_kv_heads, c.head_dim, c.ffn, c.vocab, c.n_layers);
+  a.wt = m->gv_wt; a.wt_layer_bytes = t.layer_bytes; a.wt_off_o = t.off_o; a.wt_off_gu = t.off_gu;
+  a.wt_off_down = t.off_down; a.wt_lm = m->gv_wt + t.lm_off;
+  a.embed = (const __nv_bfloat16*)m->w.embed;
+  a.norms = m->fw_norms;
+  a.cos = m->w.rope_cos; a.sin = m->w.rope_sin;
+  a.ctl = ctl;
+  a.kcache = (char*)m->kc; a.vcache = (char*)m->vc; a.kv_layer_bytes = (long long)m->kv_layer_elems * 2;
+  a.h = m->h; a.xa = m->xa_b; a.xb = m->fw_xb; a.qkv = m->qkv; a.attn_b = m->attn_b; a.act_b = m->act_b;
+  a.ss = m->gv_ss; a.attn_ws = m->gv_attn_ws; a.sync = m->gv_sync; a.best = m->fw_best;
+  a.logits = want_logits ? m->logits : nullptr;
+  a.ab_req = m->fw_ab_req; a.ab_done = m->fw_ab_done;
+  a.cuts = m->fw_sched ? fw::cut_counter(m->fw_sched) : nullptr;
+  a.d = c.d_model; a.H = c.n_heads; a.KV = c.n_kv_heads; a.hd = c.head_dim; a.ffn = c.ffn; a.vocab = c.vocab;
+  a.L = c.n_layers; a.S = c.max_seq; a.eos = c.eos_token; a.exclude_eos = c.exclude_eos;
+  a.eps = c.norm_eps; a.scale = 1.0f / sqrtf((float)c.head_dim);
+  a.stages = std::max(2, std::min(gv::max_stages(c.d_model, c.n_heads, c.n_kv_heads, c.head_dim, c.ffn),
+                                  env_int("AMUSD_GV_STAGES", 99)));
+  a.max_splits = gv::attn_splits(c.max_seq);
+  const int grid = m->fw_grid > 0 ? m->fw_grid : model_sms(m);
+  if (m->fw_dbg && (size_t)m->fw_dbg_items * 8 >= (size_t)grid * (gv::kDbgEvents + 9 * 24)) a.dbg = m->fw_dbg;
+  a.debug = env_int("AMUSD_GV_DEBUG", 0);
+  a.l2_ahead = env_int("AMUSD_GV_L2", 0);
+  CUDA_TRY(gv::launch(a, grid, st));
+  return AMUSD_OK;
+}
+
 // Enqueue one forward of `m` driven by control block `ctl` (rows <= nr).
 static int model_forward(amusd_model* m, StepCtl* ctl, int nr, cudaStream_t st, bool pdl, bool want_logits) {
   if (m->kind == 1) {
@@ -471,6 +526,7 @@ static int model_forward(amusd_model* m, StepCtl* ctl, int nr, cudaStream_t st, 
                                  m->agree_thr, m->script, m->script_len, m->eos_position, st));
     return AMUSD_OK;
   }
+  if (use_gv(m)) return gv_forward(m, ctl, st, want_logits);
   if (use_fw(m)) return fw_forward(m, ctl, st, want_logits);
   if (!m->row_major) return fail(AMUSD_ERR_UNSUPPORTED, "row-major weights released: persistent path only");
   if (use_tc(m, nr)) {
@@ -492,7 +548,7 @@ static int model_forward(amusd_model* m, StepCtl* ctl, int nr, cudaStream_t st, 
 
 static int model_kernels_per_forward(const amusd_model* m, int nr = KMAX) {
   if (m->kind == 1) return 1;
-  if (use_fw(m)) return 1;
+  if (use_persistent(m)) return 1;
   if (use_tc(m, nr)) return 1 + 5 * m->cfg.n_layers + 2;
   return 1 + 5 * m->cfg.n_layers + 2;
 }
@@ -760,12 +816,51 @@ int amusd_model_set_timeline(amusd_model* m, void* buf, size_t bytes) {
 
 int amusd_model_set_path(amusd_model* m, int path) {
   if (!m) return fail(AMUSD_ERR_INVALID_INPUT, "null model");
-  if (path < AMUSD_PATH_PERSISTENT || path > AMUSD_PATH_SIMT) return fail(AMUSD_ERR_INVALID_INPUT, "unknown path");
+  if (path < AMUSD_PATH_PERSISTENT || path > AMUSD_PATH_DECODE) return fail(AMUSD_ERR_INVALID_INPUT, "unknown path");
+  if (path == AMUSD_PATH_DECODE && (m->kind != 0 || !m->gv_ok))
+    return fail(AMUSD_ERR_UNSUPPORTED, "the decode forward needs a bf16 model with 64-multiple GEMV widths, 16-row "
+                                       "output blocks, head_dim 64/128 and <= 8 query heads per KV head");
+  if (path == AMUSD_PATH_DECODE && !m->gv_wt)
+    return fail(AMUSD_ERR_INVALID_INPUT, "attach the decode weight layout first (amusd_model_set_decode)");
   if (path != AMUSD_PATH_SIMT && m->kind == 0 && !m->tc)
     return fail(AMUSD_ERR_UNSUPPORTED, "tensor-core paths need a bf16 model with 128-aligned shapes");
   if (m->kind == 0 && path != AMUSD_PATH_PERSISTENT && !m->row_major)
     return fail(AMUSD_ERR_UNSUPPORTED, "the row-major weights were released: only the persistent path remains");
   m->path = path;
+  return AMUSD_OK;
+}
+
+size_t amusd_decode_bytes(amusd_model* m) {
+  if (!m || m->kind != 0 || !m->gv_ok) return 0;
+  const amusd_tf_config& c = m->cfg;
+  return (size_t)gv::layout(c.d_model, c.n_heads, c.n_kv_heads, c.head_dim, c.ffn, c.vocab, c.n_layers).total;
+}
+
+int amusd_model_set_decode(amusd_model* m, void* buf, size_t bytes) {
+  if (!m) return fail(AMUSD_ERR_INVALID_INPUT, "null model");
+  if (!buf) {
+    if (m->path == AMUSD_PATH_DECODE) return fail(AMUSD_ERR_INVALID_INPUT, "the decode path is selected");
+    m->gv_wt = nullptr;
+    return AMUSD_OK;
+  }
+  if (m->kind != 0 || !m->gv_ok)
+    return fail(AMUSD_ERR_UNSUPPORTED, "this model's shapes do not take the decode forward");
+  if (!m->row_major) return fail(AMUSD_ERR_UNSUPPORTED, "the row-major weights were released");
+  if (bytes < amusd_decode_bytes(m)) return fail(AMUSD_ERR_INVALID_INPUT, "decode weight buffer too small");
+  const amusd_tf_config& c = m->cfg;
+  const gv::Layout t = gv::layout(c.d_model, c.n_heads, c.n_kv_heads, c.head_dim, c.ffn, c.vocab, c.n_layers);
+  uint8_t* dst = (uint8_t*)buf;
+  const int ncols = (c.n_heads + 2 * c.n_kv_heads) * c.head_dim, hh = c.n_heads * c.head_dim;
+  for (int l = 0; l < c.n_layers; ++l) {
+    uint8_t* lw = dst + (size_t)l * t.layer_bytes;
+    CUDA_TRY(gv::tile_weights(m->w.wqkv[l], nullptr, ncols, c.d_model, lw, 0));
+    CUDA_TRY(gv::tile_weights(m->w.wo[l], nullptr, c.d_model, hh, lw + t.off_o, 0));
+    CUDA_TRY(gv::tile_weights(m->w.wgate[l], m->w.wup[l], 2 * c.ffn, c.d_model, lw + t.off_gu, 0));
+    CUDA_TRY(gv::tile_weights(m->w.wdown[l], nullptr, c.d_model, c.ffn, lw + t.off_down, 0));
+  }
+  CUDA_TRY(gv::tile_weights(m->w.lm_head, nullptr, c.vocab, c.d_model, dst + t.lm_off, 0));
+  CUDA_TRY(cudaDeviceSynchronize());
+  m->gv_wt = dst;
   return AMUSD_OK;
 }
 
@@ -1260,7 +1355,7 @@ static int capture_body(amusd_session* s, int engine, int actor, cudaGraph_t bod
   // the work-queue kernel needs no particular grid size).  Other engines own the GPU.
   const int draft_sms = std::max(1, std::min(num_sms() - 1, env_int("AMUSD_FW_DRAFT_GRID", 64)));
   for (amusd_model* m : {s->draft, s->verify}) {
-    if (!m || !use_fw(m)) continue;
+    if (!m || !use_persistent(m)) continue;
     m->fw_stages = env_int("AMUSD_FW_STAGES", fw_max_stages(m->cfg, 1));
     m->fw_grid = model_sms(m);
     if (colo) m->fw_grid = m == s->draft ? draft_sms : num_sms() - draft_sms;
@@ -1291,7 +1386,7 @@ static int capture_body(amusd_session* s, int engine, int actor, cudaGraph_t bod
   cudaGraph_t g2 = body;
   cudaError_t e = cudaStreamEndCapture(st, &g2);
   for (amusd_model* m : {s->draft, s->verify}) {  // parity API launches own the GPU again
-    if (!m || !use_fw(m)) continue;
+    if (!m || !use_persistent(m)) continue;
     m->fw_part_ok = false;
     m->fw_stages = env_int("AMUSD_FW_STAGES", fw_max_stages(m->cfg, 1));
     m->fw_grid = model_sms(m);

@@ -446,21 +446,31 @@ class TransformerModel(CudaModel):
         """Deterministic random init on the GPU: uniform with the given std, norms = 1."""
         return {n: self._synthetic_one(i, n, tdt, seed, std) for i, n in enumerate(weight_names(self.config))}
 
-    PATHS = {"persistent": L.PATH_PERSISTENT, "kernels": L.PATH_KERNELS, "simt": L.PATH_SIMT}
+    PATHS = {"persistent": L.PATH_PERSISTENT, "kernels": L.PATH_KERNELS, "simt": L.PATH_SIMT,
+             "decode": L.PATH_DECODE}
 
     def set_path(self, path: str) -> None:
-        """Select the forward implementation (perf A/B, parity tests): 'persistent'
-        (one tcgen05 launch per forward, default), 'kernels' (per-kernel tcgen05)
-        or 'simt'.  Sessions capture the path when they first launch an engine."""
+        """Select the forward implementation: 'persistent' (one tcgen05 launch per forward,
+        default), 'decode' (one persistent SIMT GEMV launch per forward -- the draft's path:
+        its forwards carry 1-2 rows), 'kernels' (per-kernel tcgen05) or 'simt'.  Sessions
+        capture the path when they first launch an engine."""
         if path not in self.PATHS:
             raise InvalidInputError(f"unknown forward path {path!r}")
+        if path == "decode" and getattr(self, "_decode_w", None) is None:
+            nbytes = self._lib.amusd_decode_bytes(self._h)
+            if nbytes == 0:
+                raise InvalidInputError("this model's shapes do not take the decode forward")
+            buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            with torch.cuda.device(self.device):
+                L.check(self._lib.amusd_model_set_decode(self._h, C.c_void_p(buf.data_ptr()), nbytes))
+            self._decode_w = buf   # decode-layout weights (~ the model's weight bytes), owned here
         L.check(self._lib.amusd_model_set_path(self._h, self.PATHS[path]))
         self.path = path
 
     def kernels_per_forward(self) -> int:
         c = self.config
         tc = c.dtype == "bf16" and c.use_tensor_cores
-        if tc and getattr(self, "path", "persistent") == "persistent":
+        if tc and getattr(self, "path", "persistent") in ("persistent", "decode"):
             return 1
         return 1 + 5 * c.n_layers + 2
 

@@ -81,5 +81,6 @@ int main() {
   // per-SM streaming rate at partial grids (the persistent forward's 10-stage ring)
   BULK(16384, 10, false, 16) BULK(16384, 10, false, 32) BULK(16384, 10, false, 84) BULK(16384, 10, false, 148)
   BULK(32768, 6, false, 16) BULK(65536, 3, false, 16)
+  BULK(16384, 11, false, 148) BULK(16384, 11, false, 64) BULK(16384, 11, false, 32)
   return 0;
 }
