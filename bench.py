@@ -54,6 +54,11 @@ def parse():
     ap.add_argument("--profile-only", action="store_true", help="one AMUSD decode, no extras (for ncu)")
     ap.add_argument("--engines", default="ar,sync,amusd", help="subset of ar,sync,amusd to time")
     ap.add_argument("--no-extras", action="store_true", help="skip roofline/e2e/cpu legs (quick sweeps)")
+    ap.add_argument("--draft-path-sync", default="decode", choices=["persistent", "decode"],
+                    help="draft forward for sync-SD (the draft owns the GPU): persistent SIMT decode kernel or the "
+                         "tcgen05 work-queue forward")
+    ap.add_argument("--draft-path-amusd", default="persistent", choices=["persistent", "decode"],
+                    help="draft forward for co-located AMUSD (the draft gets its SM share)")
     ap.add_argument("--layout", default="auto", choices=["auto", "replicas", "split", "pairs"],
                     help="N>1: auto = the paper's split pair at N=2 (draft on rank 0's GPU, verify on rank 1's: "
                          "BASELINE config 2) and independent co-located pairs per GPU otherwise (replicas); "
@@ -301,6 +306,8 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
         if name not in args.engines.split(","):
             continue
         s, eng = sess[name]
+        if name in ("sync", "amusd") and args.shapes == "1b8b":
+            dm.set_path(args.draft_path_sync if name == "sync" else args.draft_path_amusd)  # captured at graph build
         for _ in range(args.warmup):
             s.run(eng, prompt)
         per, toks, launches, stats = [], 0, 0, []

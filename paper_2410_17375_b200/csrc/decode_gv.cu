@@ -53,6 +53,7 @@ constexpr int kPad = 32;                 // ints per counter line
 constexpr int kMaxStages = 16;
 constexpr int kMaxGrid = 256;
 constexpr int kMaxG = 8;
+constexpr int kSsBlk = 8;                // residual blocks per CTA whose h^2 sums stay in shared memory
 constexpr int kSmemBudget = 232448 - 2048;  // leave room for 1-CTA protocol kernels on the SM
 constexpr long long kWaitNs = 4ll * 1000 * 1000 * 1000;
 
@@ -73,6 +74,7 @@ struct alignas(16) Aux {
   unsigned long long key[KMAX];
   float ml[4][kMaxG][2];
   float part[kCW][32][4];  // per-warp MMA partials of a K-split block
+  float ssb[kSsBlk][KMAX];  // residual phases: sum of h^2 per (owned block, activation row)
   int cut;
   int go;
   int consumed;
@@ -339,17 +341,6 @@ AMUSD_DEV void grid_arrive(const GvArgs& a, Cons& cs) {
   ++cs.ev;
 }
 
-// RMSNorm factor of every live row from the per-CTA sums of squares (fixed order).
-AMUSD_DEV void scales_from_ss(const GvArgs& a, Aux* ax, const Cons& cs) {
-  for (int r = cs.warp; r < cs.R; r += kCW) {
-    float s = 0.f;
-    for (int c = cs.lane; c < (int)gridDim.x; c += 32) s += __ldcg(a.ss + (size_t)c * KMAX + r);
-    s = warp_sum(s);
-    if (cs.lane == 0) ax->scale[r] = 1.0f / sqrtf(s / (float)a.d + a.eps);
-  }
-  named_bar(1, kCT);
-}
-
 // Layer-0 input straight from the embedding rows (no embedding phase): every CTA computes the
 // factor of each row itself and writes the residual rows it owns.
 AMUSD_DEV void embed_prologue(const GvArgs& a, Aux* ax, const Cons& cs) {
@@ -385,12 +376,37 @@ AMUSD_DEV uint4 x_global(const GvArgs& a, const bf16* src, const bf16* gamma, in
 }
 
 // Phase start: activation rows r0 .. r0 + nrows - 1 of the GEMV input into shared memory.
-AMUSD_DEV void fill_xs(const GvArgs& a, uint8_t* xs, int r0, int nrows, const bf16* src, const bf16* gamma, int K,
-                       const Cons& cs) {
+AMUSD_DEV void fill_xs(const GvArgs& a, Aux* ax, uint8_t* xs, int r0, int nrows, const bf16* src, const bf16* gamma,
+                       int K, bool scales, const Cons& cs) {
+  // the RMSNorm factors (per-CTA sums of squares of the previous residual phase) are fetched in
+  // the same round trip as the activations: issue both, then reduce
+  float ssv[(kMaxGrid + 31) / 32];
+  const int G = gridDim.x;
+  const bool sc = scales && cs.warp < cs.R;
+  if (sc) {
+#pragma unroll
+    for (int j = 0; j < (kMaxGrid + 31) / 32; ++j) {
+      const int c = cs.lane + 32 * j;
+      ssv[j] = c < G ? __ldcg(a.ss + (size_t)c * KMAX + cs.warp) : 0.f;
+    }
+  }
   const int n8 = K / 8;
   for (int i = cs.ct; i < nrows * n8; i += kCT) {
     const int r = i / n8, k = (i % n8) * 8;
     *(uint4*)(xs + (size_t)r * xs_pitch(K) + k * 2) = x_global(a, src, gamma, K, r0 + r, k);
+  }
+  if (scales) {
+    for (int r = cs.warp; r < cs.R; r += kCW) {
+      float s = 0.f;
+      if (r == cs.warp) {
+#pragma unroll
+        for (int j = 0; j < (kMaxGrid + 31) / 32; ++j) s += ssv[j];
+      } else {  // > 8 live rows: the extra rows in a second round trip
+        for (int c = cs.lane; c < G; c += 32) s += __ldcg(a.ss + (size_t)c * KMAX + r);
+      }
+      s = warp_sum(s);
+      if (cs.lane == 0) ax->scale[r] = 1.0f / sqrtf(s / (float)a.d + a.eps);
+    }
   }
   named_bar(1, kCT);
 }
@@ -452,6 +468,7 @@ AMUSD_DEV void block_epilogue(const GvArgs& a, Aux* ax, int kind, int l, int b, 
                               const float (&hpre)[4], const Cons& cs) {
   const int g = cs.lane >> 2, q = cs.lane & 3;
   unsigned long long best[2] = {0ull, 0ull};
+  float sq[2] = {0.f, 0.f};  // residual phases: this lane's sum of h^2 per activation row (rows g, g + 8)
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const int row = g + 8 * (e >> 1), r = r0 + 2 * q + (e & 1);
@@ -467,6 +484,7 @@ AMUSD_DEV void block_epilogue(const GvArgs& a, Aux* ax, int kind, int l, int b, 
       case kDown: {
         const int n = b * kMB + row;
         const float hn = hpre[e] + acc;
+        sq[e & 1] = fmaf(hn, hn, sq[e & 1]);
         a.h[(size_t)r * a.d + n] = hn;
         const bf16* gam = a.norms + (size_t)(kind == kO ? 2 * l + 1 : 2 * l + 2) * a.d;
         bf16* xn = kind == kO ? a.xb : a.xa;
@@ -490,6 +508,17 @@ AMUSD_DEV void block_epilogue(const GvArgs& a, Aux* ax, int kind, int l, int b, 
       }
     }
   }
+  if (kind == kO || kind == kDown) {  // block's sum of squares per activation row, fixed shuffle tree
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float v = sq[h];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      const int r = r0 + 2 * q + h;
+      if (g == 0 && r < cs.R) ax->ssb[b % kSsBlk][r] = v;
+    }
+  }
   if (kind == kLm) {  // max over the lanes holding the same activation row, one smem atomic
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -508,7 +537,7 @@ AMUSD_DEV void block_epilogue(const GvArgs& a, Aux* ax, int kind, int l, int b, 
 // One GEMV phase: passes of up to 8 activation rows (one pass for the draft's 1-2 rows; more
 // rows than shared memory holds: several passes, each re-streaming the phase's units).
 __device__ __noinline__ void gemv_phase(const GvArgs& a, Aux* ax, uint8_t* ring, uint8_t* xs, int kind, int l,
-                                        const bf16* src, const bf16* gamma, Cons& cs) {
+                                        const bf16* src, const bf16* gamma, bool scales, Cons& cs) {
   const WPhase p = wphase_of(a, kind, l);
   const int nb = p.b1 - p.b0;
   const bool resid = kind == kO || kind == kDown;
@@ -528,7 +557,7 @@ __device__ __noinline__ void gemv_phase(const GvArgs& a, Aux* ax, uint8_t* ring,
   const int groups = kCW / S, js = cs.warp / S, qs = cs.warp % S;
   for (int ps = 0; ps < npass; ++ps) {
     const int r0 = ps * cap, nx = min(cap, cs.R - r0);
-    fill_xs(a, xs, r0, nx, src, gamma, p.K, cs);
+    fill_xs(a, ax, xs, r0, nx, src, gamma, p.K, scales && ps == 0, cs);
     if (pm) { const long long t = clock64(); pm[0] += t - tp0; tp0 = t; }
     for (int j = js; j < nb; j += groups) {
       const int b = p.b0 + j;
@@ -575,18 +604,23 @@ __device__ __noinline__ void gemv_phase(const GvArgs& a, Aux* ax, uint8_t* ring,
   }
 }
 
-// Sum of squares of the residual rows this CTA owns (fixed order), for the next RMSNorm.
-AMUSD_DEV void publish_ss(const GvArgs& a, const Cons& cs) {
+// Sum of squares of the residual rows this CTA owns, for the next RMSNorm: the blocks' sums the
+// epilogues left in shared memory, added in block order (no re-read of h).
+AMUSD_DEV void publish_ss(const GvArgs& a, Aux* ax, const Cons& cs) {
   int n0, n1;
   own_rows(a.d, n0, n1);
-  for (int r = cs.warp; r < cs.R; r += kCW) {
+  const int b0 = n0 / kMB, nb = (n1 - n0) / kMB;
+  for (int r = cs.ct; r < cs.R; r += kCT) {
     float s = 0.f;
-    for (int n = n0 + cs.lane; n < n1; n += 32) {
-      const float v = __ldcg(a.h + (size_t)r * a.d + n);
-      s = fmaf(v, v, s);
+    if (nb <= kSsBlk) {
+      for (int j = 0; j < nb; ++j) s += ax->ssb[(b0 + j) % kSsBlk][r];
+    } else {
+      for (int n = n0; n < n1; ++n) {
+        const float v = __ldcg(a.h + (size_t)r * a.d + n);
+        s = fmaf(v, v, s);
+      }
     }
-    s = warp_sum(s);
-    if (cs.lane == 0) a.ss[(size_t)blockIdx.x * KMAX + r] = s;
+    a.ss[(size_t)blockIdx.x * KMAX + r] = s;
   }
 }
 
@@ -689,42 +723,35 @@ __device__ __noinline__ bool attn_phase(const GvArgs& a, Aux* ax, uint8_t* un, i
       cp_async_wait_all();
       named_bar(1, kCT);
       mark(0);
-      // 3) scores: thread = (position, head parity); the K row is read once per head pair
-      {
-        const int pi = ct % kChunk, t = lo + pi;
-        uint4 kv[HD / 8];
-        if (t < hi) {
+      // 3) scores: thread = (position, query head) pair (a quad of lanes shares the K row)
+      for (int pr = ct; pr < (hi - lo) * G; pr += kCT) {
+        const int pi = pr / G, jh = pr % G, t = lo + pi;
+        const uint4* kr = (const uint4*)(ksp + pi * PITCH);
+        float dot[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-          for (int c = 0; c < HD / 8; ++c) kv[c] = *((const uint4*)(ksp + pi * PITCH) + c);
-        }
-        for (int jh = ct / kChunk; jh < G; jh += kCT / kChunk) {
-          float dot[4] = {0.f, 0.f, 0.f, 0.f};
-          if (t < hi) {
-#pragma unroll
-            for (int c = 0; c < HD / 8; ++c) {
-              const F8 f8 = unpack8(kv[c]);
-              const float* f = f8.v;
-#pragma unroll
-              for (int rr = 0; rr < 4; ++rr) {
-                if (rr < nrg) {
-                  const float4* q4 = (const float4*)(qs + (rr * G + jh) * HD + c * 8);
-                  const float4 qa = q4[0], qb = q4[1];
-                  float d = dot[rr];
-                  d = fmaf(qa.x, f[0], d); d = fmaf(qa.y, f[1], d); d = fmaf(qa.z, f[2], d); d = fmaf(qa.w, f[3], d);
-                  d = fmaf(qb.x, f[4], d); d = fmaf(qb.y, f[5], d); d = fmaf(qb.z, f[6], d); d = fmaf(qb.w, f[7], d);
-                  dot[rr] = d;
-                }
-              }
-            }
-          }
+        for (int c = 0; c < HD / 8; ++c) {
+          const F8 f8 = unpack8(kr[c]);
+          const float* f = f8.v;
 #pragma unroll
           for (int rr = 0; rr < 4; ++rr) {
             if (rr < nrg) {
-              const bool ok = t < hi && t <= cs.pos0 + rg0 + rr;
-              sc[(rr * G + jh) * kChunk + pi] = ok ? dot[rr] * a.scale : -INFINITY;
+              const float4* q4 = (const float4*)(qs + (rr * G + jh) * HD + c * 8);
+              const float4 qa = q4[0], qb = q4[1];
+              float d = dot[rr];
+              d = fmaf(qa.x, f[0], d); d = fmaf(qa.y, f[1], d); d = fmaf(qa.z, f[2], d); d = fmaf(qa.w, f[3], d);
+              d = fmaf(qb.x, f[4], d); d = fmaf(qb.y, f[5], d); d = fmaf(qb.z, f[6], d); d = fmaf(qb.w, f[7], d);
+              dot[rr] = d;
             }
           }
         }
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr)
+          if (rr < nrg) sc[(rr * G + jh) * kChunk + pi] = t <= cs.pos0 + rg0 + rr ? dot[rr] * a.scale : -INFINITY;
+      }
+      for (int i = ct; i < G * kChunk; i += kCT) {  // positions past the chunk's end
+        const int jh = i / kChunk, pi = i % kChunk;
+        if (pi >= hi - lo)
+          for (int rr = 0; rr < nrg; ++rr) sc[(rr * G + jh) * kChunk + pi] = -INFINITY;
       }
       named_bar(1, kCT);
       mark(1);
@@ -854,30 +881,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_decode(const __grid_constant__ 
     embed_prologue(a, ax, cs);
     for (int l = 0; l < a.L && ok; ++l) {
       const bf16* gamma_attn = a.norms + (size_t)(2 * l) * a.d;
-      if (l > 0) {
-        if (!(ok = grid_wait(a, ax, cs))) break;
-        scales_from_ss(a, ax, cs);
-      }
-      gemv_phase(a, ax, ring, xs, kQkv, l, l == 0 ? nullptr : a.xa, gamma_attn, cs);
+      if (l > 0 && !(ok = grid_wait(a, ax, cs))) break;
+      gemv_phase(a, ax, ring, xs, kQkv, l, l == 0 ? nullptr : a.xa, gamma_attn, l > 0, cs);
       grid_arrive(a, cs);
       if (!(ok = attn_phase<HD>(a, ax, un, l, cs))) break;
       grid_arrive(a, cs);
       if (!(ok = grid_wait(a, ax, cs))) break;
-      gemv_phase(a, ax, ring, xs, kO, l, a.attn_b, nullptr, cs);
-      publish_ss(a, cs);
+      gemv_phase(a, ax, ring, xs, kO, l, a.attn_b, nullptr, false, cs);
+      publish_ss(a, ax, cs);
       grid_arrive(a, cs);
       if (!(ok = grid_wait(a, ax, cs))) break;
-      scales_from_ss(a, ax, cs);
-      gemv_phase(a, ax, ring, xs, kGu, l, a.xb, nullptr, cs);
+      gemv_phase(a, ax, ring, xs, kGu, l, a.xb, nullptr, true, cs);
       grid_arrive(a, cs);
       if (!(ok = grid_wait(a, ax, cs))) break;
-      gemv_phase(a, ax, ring, xs, kDown, l, a.act_b, nullptr, cs);
-      publish_ss(a, cs);
+      gemv_phase(a, ax, ring, xs, kDown, l, a.act_b, nullptr, false, cs);
+      publish_ss(a, ax, cs);
       grid_arrive(a, cs);
     }
     if (ok && (ok = grid_wait(a, ax, cs))) {
-      scales_from_ss(a, ax, cs);
-      gemv_phase(a, ax, ring, xs, kLm, 0, a.xa, nullptr, cs);
+      gemv_phase(a, ax, ring, xs, kLm, 0, a.xa, nullptr, true, cs);
       if (cs.ct == 0) {
         for (int r = 0; r < cs.R; ++r) atomicMax(a.best + r, ax->key[r]);
         __threadfence();
