@@ -382,11 +382,27 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
     def fwd_bytes(c, rows):
         return c.step_weight_bytes() + c.kv_bytes_per_token() * (ctx + rows)
     kernels = {}
+    dm.set_path("persistent")
     for key, m, c, rows, iters in (("verify_forward_m1", vm, vcfg, 1, 10), ("verify_forward_m4", vm, vcfg, 4, 10),
                                    ("verify_forward_m16", vm, vcfg, 16, 5), ("draft_forward_m1", dm, dcfg, 1, 20)):
         ms = time_fwd(m, rows, -1, iters=iters)
         b = fwd_bytes(c, rows)
         kernels[key] = {"bytes": b, "ms": ms, "gbs": b / ms / 1e6}
+    if args.shapes == "1b8b":  # the draft through the persistent SIMT/mma decode forward (decode_gv.cu)
+        dm.set_path("decode")
+        ms = time_fwd(dm, 1, -1, iters=20)
+        b = fwd_bytes(dcfg, 1)
+        kernels["draft_forward_m1_decode"] = {"bytes": b, "ms": ms, "gbs": b / ms / 1e6}
+        dm.set_path("persistent")
+    # the verify forward at the run's mean context (the AR loop decodes from ctx P to P + N): the
+    # per-step protocol cost = AR ms/token over this
+    ctx_mean = Plen + N // 2
+    st = vm.init_state(synthetic_prompt(ctx_mean, vcfg.vocab_size))
+    ms_mean = time_fwd(vm, 1, -1, iters=10)
+    kernels[f"verify_forward_m1_ctx{ctx_mean}"] = {"bytes": vcfg.step_weight_bytes() + vcfg.kv_bytes_per_token() * (ctx_mean + 1),
+                                                   "ms": ms_mean, "gbs": 0.0}
+    kernels[f"verify_forward_m1_ctx{ctx_mean}"]["gbs"] = kernels[f"verify_forward_m1_ctx{ctx_mean}"]["bytes"] / ms_mean / 1e6
+    st = vm.init_state(prompt)
     traffic = None
     prof = ROOT / "profiles" / "dominant_kernel_traffic.json"
     if prof.exists():
@@ -399,6 +415,8 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
                 "algorithmic_bytes_per_launch": int(dom["bytes"]), "peak_source": peak_src,
                 "forwards": {k: {"ms": round(v["ms"], 4), "GB/s": round(v["gbs"], 1), "bytes": int(v["bytes"]),
                                  "frac": round(v["gbs"] / hbm_peak, 4)} for k, v in kernels.items()}}
+    if "ar" in results:  # protocol + graph-loop cost per AR step over the isolated forward at the mean context
+        roofline["ar_step_over_forward"] = round(results["ar"]["ms_per_token"] / ms_mean - 1.0, 4)
     # ---- end to end through the public API (host prompt in, host tokens out, wall clock)
     e2e = None
     if rank == 0 or world > 1:

@@ -303,6 +303,7 @@ AMUSD_DEV void resid_prefetch(const GemmKind& ph, const __nv_bfloat16* gnext, in
                  "l"(gnext + t * BM + nl * 8) : "memory");
 }
 
+template <bool TP>
 AMUSD_DEV void tile_epilogue(const FwArgs& a, const GemmKind& ph, const __nv_bfloat16* gnext, int t, int nl,
                              const float (&v)[BN], int rows, EpiSmem* es, EpiTmp* et, int q, int lane) {
   const float* inv = es->inv;
@@ -364,7 +365,7 @@ AMUSD_DEV void tile_epilogue(const FwArgs& a, const GemmKind& ph, const __nv_bfl
     if (q == 0 && lane < BN && lane < rows) {
       unsigned long long b = et->kx[lane];
       for (int w = 1; w < 4; ++w) b = et->kx[w * BN + lane] > b ? et->kx[w * BN + lane] : b;
-      if (a.tp > 1) {  // every rank's keys (order-independent max: the all-rank argmax everywhere)
+      if (TP && a.tp > 1) {  // every rank's keys (order-independent max: the all-rank argmax everywhere)
         for (int p = 0; p < a.tp; ++p) atomicMax_system(a.peer_best[p] + lane, b);
       } else {
         atomicMax(a.best + lane, b);
@@ -800,7 +801,10 @@ constexpr int attn_scratch_bytes() {
 }
 constexpr int epi_bytes() { return ((int)sizeof(EpiSmem) + 127) & ~127; }
 
-template <int HD, int G, int MINB>
+// TP: a tensor-parallel shard's instance (cross-rank split-K reduce, all-rank argmax).  The
+// unsharded instance compiles those branches out: as runtime checks in the split-K path they
+// cost 8% (8B) / 17% (1B) of the forward.
+template <int HD, int G, int MINB, bool TP>
 __global__ void __launch_bounds__(kThreads, MINB)
     k_forward(const __grid_constant__ CUtensorMap m_xa, const __grid_constant__ CUtensorMap m_attn,
               const __grid_constant__ CUtensorMap m_act, const __grid_constant__ CUtensorMap m_xb,
@@ -1190,7 +1194,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         const int cj = j / g.ntiles, t = j - cj * g.ntiles;
         bool final = true;
         float acc[BN];
-        if (nchunks > 1 || g.xr) {
+        if (nchunks > 1 || (TP && g.xr)) {
           // Split-K in exact int64 fixed point (2^-32): the red.adds commute, so the merged
           // tile is bit-identical whatever the chunks' arrival order (deterministic, batch
           // invariant) and no partial ever needs a merge round trip.  Layout [tile][row][128].
@@ -1201,7 +1205,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           for (int r = 0; r < BN; ++r) {
             if (r < L.rows) {
               const long long fx = __float2ll_rn(v[r] * 4294967296.0f);
-              if (g.xr) {  // tensor parallel: into every rank's accumulator (the fused allreduce)
+              if (TP && g.xr) {  // tensor parallel: into every rank's accumulator (the fused allreduce)
                 for (int pr = 0; pr < a.tp; ++pr) red_add_u64_sys(a.peer_ws[pr] + off + r * BM, fx);
               } else {
                 asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(acc64 + r * BM), "l"(fx) : "memory");
@@ -1215,12 +1219,12 @@ __global__ void __launch_bounds__(kThreads, MINB)
           // a system-scope fence; each rank's local last chunk merges once all ranks' chunks
           // have arrived.
           final = cj == nchunks - 1;
-          if (g.xr && tid == 0) {
+          if (TP && g.xr && tid == 0) {
             __threadfence_system();
             for (int pr = 0; pr < a.tp; ++pr) red_add_sys(a.peer_cnt[pr] + g.cnt_off + t * kPad, 1);
           }
           if (!final) {
-            if (tid == 0 && !g.xr) {
+            if (tid == 0 && !(TP && g.xr)) {
               if (a.debug & 32) red_add_relaxed(a.tile_cnt + g.cnt_off + t * kPad, 1);  // timing experiment only
               else red_add_release(a.tile_cnt + g.cnt_off + t * kPad, 1);
             }
@@ -1233,7 +1237,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
               cp_async_wait_all();  // (lands while tid 0 awaits the count; others wait at the barrier)
             }
             if (tid == 0) {
-              if (g.xr) wait_count_sys(a.tile_cnt + g.cnt_off + t * kPad, g.nchunks_total);
+              if (TP && g.xr) wait_count_sys(a.tile_cnt + g.cnt_off + t * kPad, g.nchunks_total);
               else wait_count(a.tile_cnt + g.cnt_off + t * kPad, nchunks - 1);
               a.tile_cnt[g.cnt_off + t * kPad] = 0;  // re-arm for the next phase / launch
               if (a.dbg) dbg_mark(a, phase_first(a, L, p) + j, 6, globaltimer());
@@ -1259,7 +1263,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         }
         if (final) {
           const __nv_bfloat16* gnext = g.gnext ? g.gnext + (size_t)layer * g.gnext_stride : nullptr;
-          tile_epilogue(a, g, gnext, t, nl, acc, L.rows, es, et, q, lane);
+          tile_epilogue<TP>(a, g, gnext, t, nl, acc, L.rows, es, et, q, lane);
         }
         wrote = final;
         lm_last_check = epi == kEpArgmax;
@@ -1307,13 +1311,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
       if (tid == 0) {
         if (a.dbg) dbg_mark(a, phase_first(a, L, p) + j, 5, globaltimer());
         if (lm_last_check) {
-          if (a.tp > 1) {  // this item's keys reached every rank: count it everywhere
+          if (TP && a.tp > 1) {  // this item's keys reached every rank: count it everywhere
             __threadfence_system();
             for (int pr = 0; pr < a.tp; ++pr) red_add_sys(lm_counter(a.peer_sched[pr]), 1);
           }
           const int old = atom_add_acq_rel(done + p * kPad, 1);
           if (old == a.g[kGLm].nitems - 1) {  // last LM-head item: final argmax per row
-            if (a.tp > 1) {  // ... once every rank's LM items have merged their keys here
+            if (TP && a.tp > 1) {  // ... once every rank's LM items have merged their keys here
               wait_count_sys(lm_counter(a.sched), a.lm_items_total);
               *lm_counter(a.sched) = 0;
             }
@@ -1517,7 +1521,11 @@ bool build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_f
   a->g[kGDown].gnext = m.norms + 2 * m.d;   // attention RMSNorm of layer l+1 at 2l+2 (final norm at 2L)
   a->g[kGDown].gnext_stride = 2 * m.d;
   a->g[kGLm] = kind(kEpArgmax, 0, m.vocab / BM, m.d, m.vocab, m.vocab, m.wt_lm, 0, "LM");
-  for (int k : {kGO, kGDown, kGQkv, kGGu, kGLm}) place_ws(a->g[k]);
+  if (m.tp > 1) {
+    for (int k : {kGO, kGDown, kGQkv, kGGu, kGLm}) place_ws(a->g[k]);
+  } else {  // unsharded: construction order
+    for (int k : {kGQkv, kGO, kGGu, kGDown, kGLm}) place_ws(a->g[k]);
+  }
   a->g[kGLm].ssp_in = m.ssp;
   a->L = m.L;
   a->attn_max = attn_items_max(m.KV, m.S);
@@ -1545,15 +1553,15 @@ int forward_smem_bytes(int stages, int hd, int group) {
   return 1024 + stages * (kStageW + kStageX) + sc + ((ctl + 127) & ~127);
 }
 
-template <int HD, int G, int MINB>
+template <int HD, int G, int MINB, bool TP>
 static cudaError_t launch_m(const FwArgs& a, const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& m2,
                             const CUtensorMap& m3, int grid, int stages, cudaStream_t st) {
   const int smem = forward_smem_bytes(stages, HD, G);
   static SmemOptIn opt;  // per device (one process may hold models on two GPUs)
-  if (cudaError_t e = opt.ensure(k_forward<HD, G, MINB>, smem)) return e;
+  if (cudaError_t e = opt.ensure(k_forward<HD, G, MINB, TP>, smem)) return e;
   FwArgs b = a;
   b.stages = stages;
-  k_forward<HD, G, MINB><<<grid, kThreads, smem, st>>>(m0, m1, m2, m3, b);
+  k_forward<HD, G, MINB, TP><<<grid, kThreads, smem, st>>>(m0, m1, m2, m3, b);
   return cudaGetLastError();
 }
 
@@ -1562,9 +1570,10 @@ static cudaError_t launch_m(const FwArgs& a, const CUtensorMap& m0, const CUtens
 template <int HD, int G>
 static cudaError_t launch_t(const FwArgs& a, const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& m2,
                             const CUtensorMap& m3, int grid, int stages, cudaStream_t st) {
+  if (a.tp > 1) return launch_m<HD, G, 1, true>(a, m0, m1, m2, m3, grid, stages, st);
   if (forward_smem_bytes(stages, HD, G) <= 232448 / 2 - 1024)
-    return launch_m<HD, G, 2>(a, m0, m1, m2, m3, grid, stages, st);
-  return launch_m<HD, G, 1>(a, m0, m1, m2, m3, grid, stages, st);
+    return launch_m<HD, G, 2, false>(a, m0, m1, m2, m3, grid, stages, st);
+  return launch_m<HD, G, 1, false>(a, m0, m1, m2, m3, grid, stages, st);
 }
 
 cudaError_t launch_forward(const FwArgs& a, const CUtensorMap& m_xa, const CUtensorMap& m_attn,
