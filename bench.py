@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--profile-only", action="store_true", help="one AMUSD decode, no extras (for ncu)")
     ap.add_argument("--engines", default="ar,sync,amusd", help="subset of ar,sync,amusd to time")
     ap.add_argument("--no-extras", action="store_true", help="skip roofline/e2e/cpu legs (quick sweeps)")
-    ap.add_argument("--draft-path-sync", default="decode", choices=["persistent", "decode"],
+    ap.add_argument("--draft-path-sync", default="persistent", choices=["persistent", "decode"],
                     help="draft forward for sync-SD (the draft owns the GPU): persistent SIMT decode kernel or the "
                          "tcgen05 work-queue forward")
     ap.add_argument("--draft-path-amusd", default="persistent", choices=["persistent", "decode"],
