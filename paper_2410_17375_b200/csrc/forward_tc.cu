@@ -728,15 +728,25 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
     *cnt = 0;
   }
   named_bar(1, 128);
-  // Merge: (1) every split's (m, l) into shared memory (one round trip; this split's own
-  // from shared memory), (2) M = max m, weights w_s = exp(m_s - M), L = sum l_s w_s in split
-  // order, (3) O = sum o_s w_s in split order, 8 splits' loads in flight per batch.
-  // Deterministic and position-only (batch invariant).
+  // Merge in ONE round trip: the first 8 remote splits' o values (registers) and every split's
+  // (m, l) (shared memory; this split's own from its stats) are issued together; then
+  // M = max m, weights w_s = exp(m_s - M), L = sum l_s w_s in split order, O = sum o_s w_s in
+  // split order (further batches of 8 splits: one more round trip each).  Deterministic and
+  // position-only (batch invariant).
   const float* base = a.attn_ws + ((size_t)g * KMAX + r) * a.max_splits * G * (HD + 2);
   // [kMaxMerge][G] m (then the weights) and l, in the V staging buffer (dead after P.V)
   float* wts = (float*)&sm->vb[0][0];
   float* mlv = wts + kMaxMerge * G;
   static_assert(2 * kMaxMerge * G * 4 <= kAttnChunk * HD * 2, "merge scratch alias");
+  constexpr int II = G * HD / 128;
+  const int nrem = nsplit - 1;
+  float o[II][8];
+#pragma unroll
+  for (int ii = 0; ii < II; ++ii) {
+    const int i = tid + 128 * ii, j = i / HD, e = i - j * HD;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) o[ii][u] = u < nrem ? __ldcg(base + ((size_t)u * G + j) * (HD + 2) + e) : 0.f;
+  }
   for (int i = tid; i < nsplit * G; i += 128) {
     const int sp = i / G, j = i - sp * G;
     float m, l;
@@ -764,25 +774,25 @@ AMUSD_DEV void attn_item(const FwArgs& a, AttnSmem<HD, G>* sm, bool staged, uint
     sm->stat[1][tid] = Ls;  // (own stat no longer needed)
   }
   named_bar(1, 128);
-  constexpr int II = G * HD / 128;
   float O[II];
 #pragma unroll
   for (int ii = 0; ii < II; ++ii) O[ii] = 0.f;
-  for (int b0 = 0; b0 < nsplit - 1; b0 += 8) {  // remote splits
-    float o[II][8];
+  for (int b0 = 0; b0 < nrem; b0 += 8) {  // remote splits in batches of 8 (the first already loaded)
+    if (b0 > 0) {
 #pragma unroll
-    for (int ii = 0; ii < II; ++ii) {
-      const int i = tid + 128 * ii, j = i / HD, e = i - j * HD;
+      for (int ii = 0; ii < II; ++ii) {
+        const int i = tid + 128 * ii, j = i / HD, e = i - j * HD;
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        o[ii][u] = b0 + u < nsplit - 1 ? __ldcg(base + ((size_t)(b0 + u) * G + j) * (HD + 2) + e) : 0.f;
+        for (int u = 0; u < 8; ++u)
+          o[ii][u] = b0 + u < nrem ? __ldcg(base + ((size_t)(b0 + u) * G + j) * (HD + 2) + e) : 0.f;
+      }
     }
 #pragma unroll
     for (int ii = 0; ii < II; ++ii) {
       const int j = (tid + 128 * ii) / HD;
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        if (b0 + u < nsplit - 1) O[ii] = fmaf(o[ii][u], wts[(b0 + u) * G + j], O[ii]);
+        if (b0 + u < nrem) O[ii] = fmaf(o[ii][u], wts[(b0 + u) * G + j], O[ii]);
     }
   }
 #pragma unroll
