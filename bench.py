@@ -351,6 +351,15 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
             "rollbacks": statistics.mean(i.rollbacks for i in stats),
             "drafted": statistics.mean(i.drafted for i in stats),
         }
+        # in-situ HBM bandwidth of the run: forwards issued x their algorithmic bytes over the
+        # device time (AMUSD: every draft forward launched, cut ones counted in full -> upper bound)
+        vfw = statistics.mean(i.verify_steps for i in stats)
+        dfw = statistics.mean((i.draft_iters if name == "amusd" else i.drafted) for i in stats) if name != "ar" else 0.0
+        ctx_m = Plen + N // 2
+        gb = (vfw * (vcfg.step_weight_bytes() + vcfg.kv_bytes_per_token() * ctx_m) +
+              dfw * (dcfg.step_weight_bytes() + dcfg.kv_bytes_per_token() * ctx_m)) / 1e9
+        results[name]["in_situ"] = {"verify_forwards": vfw, "draft_forwards": dfw, "GB_per_token": round(gb / N, 3),
+                                    "GB_per_s": round(gb / (total_ms / args.steps / 1000.0), 1)}
     variants = None
     if not args.no_extras and world == 1:
         variants = engine_variants(args, P, L, DeviceSession, finalize_tokens, dm, vm, prompt, canon, N, Plen, ref_tokens)
@@ -669,9 +678,9 @@ def main():
                            "max_window": args.window, "new_tokens": args.new_tokens,
                            "prompt_len": args.prompt_len, "parallelism": f"replicas x{world}" if world > 1 else "co-located pair",
                            "l2": "weights (17.5 GB) >> 126 MB L2: no flush needed"},
-                "amusd": {k: round(v, 3) for k, v in a.items()},
-                "sync_sd": {k: round(v, 3) for k, v in sy.items()},
-                "ar": {k: round(v, 3) for k, v in ar.items()},
+                "amusd": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in a.items()},
+                "sync_sd": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in sy.items()},
+                "ar": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in ar.items()},
                 "speedup_vs_sync": round(a["tokens_per_s"] / sy["tokens_per_s"], 3),
                 "speedup_vs_ar": round(a["tokens_per_s"] / ar["tokens_per_s"], 3),
                 "variants": out.get("variants"), "calibration": out.get("calibration"),

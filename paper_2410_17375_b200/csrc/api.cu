@@ -1359,6 +1359,12 @@ static int capture_body(amusd_session* s, int engine, int actor, cudaGraph_t bod
     m->fw_stages = env_int("AMUSD_FW_STAGES", fw_max_stages(m->cfg, 1));
     m->fw_grid = model_sms(m);
     if (colo) m->fw_grid = m == s->draft ? draft_sms : num_sms() - draft_sms;
+    // AMUSD_FW_COLO_SHARED=1 (experiment): both forwards on every SM, rings sized for two CTAs
+    // per SM (the work-queue kernel needs no co-residency, so any overlap is safe)
+    if (colo && env_int("AMUSD_FW_COLO_SHARED", 0)) {
+      m->fw_grid = model_sms(m);
+      m->fw_stages = env_int("AMUSD_FW_STAGES", fw_max_stages(m->cfg, 2));
+    }
     m->fw_part_ok = colo && m == s->draft;
   }
   auto fwd = [&](amusd_model* m, StepCtl* c, int nr) { if (!r) r = model_forward(m, c, nr, st, pdl, false); };
