@@ -201,12 +201,47 @@ def split_arm(args, rank: int, world: int, local_rank: int):
         r2, _ = decode_speculative_async_split(model, prompt, cfg, link=link, max_window=args.window)
         e2e_ms.append((time.perf_counter() - t0) * 1000.0)
         e2e_toks += len(r2.tokens)
+    # the baselines on the SAME GPUs: AR and sync-SD (k) on the verify GPU with a draft replica
+    # there (sync-SD is sequential: a second GPU gives it nothing but a cross-GPU handoff)
+    base_lines = None
+    if link.role == "verify" and not args.no_extras:
+        from paper_2410_17375_b200.engines import DeviceSession, canonical_path, finalize_tokens
+        rep = P.TransformerModel(TC.llama_1b(max_seq=max_seq), seed=1, device=dev, keep_row_major=False)
+        if torch.cuda.device_count() < world:
+            rep.set_max_grid(torch.cuda.get_device_properties(dev).multi_processor_count // max(1, world // torch.cuda.device_count()))
+        canon = canonical_path(base, prompt, N + L.KMAX)
+        base_lines = {}
+        for name, sess, eng in (("ar", DeviceSession(None, base, Plen, cfg), L.ENGINE_AR),
+                                ("sync_sd", DeviceSession(P.AgreementDraft(rep, args.rho, coin_seed=1234), base, Plen, cfg,
+                                                          canon=canon), L.ENGINE_SYNC)):
+            for _ in range(max(1, args.warmup)):
+                base.init_state(prompt)
+                rep.init_state(prompt)
+                sess.run(eng, prompt)
+            ms, nt = 0.0, 0
+            for _ in range(args.steps):
+                base.init_state(prompt)
+                rep.init_state(prompt)
+                sess.prepare(prompt)
+                st_, en_ = sess.launch(eng)
+                out = sess.collect(st_, en_)
+                toks_b, _ = finalize_tokens(out.verified, base.eos_token, N)
+                if toks_b != ref_tokens[:len(toks_b)]:
+                    raise SystemExit(f"split arm {name} output differs from AMUSD's -- parity broken")
+                ms += out.device_ms
+                nt += len(toks_b)
+            base_lines[name] = {"tokens_per_s": round(nt / (ms / 1000.0), 3), "ms_per_token": round(ms / nt, 4),
+                                "gpus": "the verify GPU (draft replica co-resident)" if name == "sync_sd" else "the verify GPU"}
+        del rep
+        P.engines.clear_sessions()
+        torch.cuda.empty_cache()
     # per-GPU roofline: each GPU's persistent forward alone (1 row) at the prompt's context
     base.init_state(prompt)
     fms = CB.forward_ms(base, 1, iters=20)
     fbytes = cfg_m.step_weight_bytes() + cfg_m.kv_bytes_per_token() * (Plen + 1)
     vrows = {m: CB.forward_ms(base, m) for m in (1, 2, 4, 8, 16)} if link.role == "verify" else None
     mine = {"rank": rank, "role": link.role, "ms": fms, "bytes": fbytes, "vrows": vrows, "toks": toks,
+            "base_lines": base_lines,
             "total": total, "prefill": max(prefill), "e2e_ms": sum(e2e_ms), "e2e_toks": e2e_toks,
             "launches": launches, "clocks": cm.summary(), "verify_steps": res.stats.verify_steps,
             "rollbacks": res.stats.rollbacks, "drafted": res.stats.drafted_tokens}
@@ -247,6 +282,9 @@ def split_arm(args, rank: int, world: int, local_rank: int):
         "amusd": {"tokens_per_s": round(v, 3), "tokens_per_s_per_pair": round(v / npairs, 3),
                   "verify_steps": vr0["verify_steps"], "rollbacks": vr0["rollbacks"], "drafted": vr0["drafted"],
                   "tokens_equal_ar": bool(ar_ok)},
+        "sync_sd": (vr0["base_lines"] or {}).get("sync_sd"), "ar": (vr0["base_lines"] or {}).get("ar"),
+        "speedup_vs_sync": round(v / npairs / vr0["base_lines"]["sync_sd"]["tokens_per_s"], 3) if vr0["base_lines"] else None,
+        "speedup_vs_ar": round(v / npairs / vr0["base_lines"]["ar"]["tokens_per_s"], 3) if vr0["base_lines"] else None,
         "prefill_ms": {"max_over_gpus": round(max(r["prefill"] for r in allr), 3),
                        "draft": round(max(r["prefill"] for r in draft_ranks), 3),
                        "verify": round(max(r["prefill"] for r in verify_ranks), 3),
