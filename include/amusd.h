@@ -157,15 +157,23 @@ int amusd_peer_enable(int device, int peer);
  * 1 = per-kernel tcgen05 path (1 + 5L + 2 launches), 2 = SIMT GEMV path,
  * 3 = persistent SIMT decode forward (decode_gv.cu: one launch, static
  *     per-CTA row partitions, fused RMSNorm + GEMV over the row-major weights;
- *     the draft model's path -- its forwards carry 1-2 rows).
+ *     the draft model's path -- its forwards carry 1-2 rows),
+ * 4 = cluster decode forward (decode_cl.cu: one 8-CTA cluster per KV head
+ *     does QKV + attention + the O slice with DSMEM hand-offs, two grid-wide
+ *     dependencies per layer; <= 8 rows per forward).
  * Applies to launches enqueued afterwards (sessions capture it per engine). */
-enum { AMUSD_PATH_PERSISTENT = 0, AMUSD_PATH_KERNELS = 1, AMUSD_PATH_SIMT = 2, AMUSD_PATH_DECODE = 3 };
+enum { AMUSD_PATH_PERSISTENT = 0, AMUSD_PATH_KERNELS = 1, AMUSD_PATH_SIMT = 2, AMUSD_PATH_DECODE = 3,
+       AMUSD_PATH_CLUSTER = 4 };
 int amusd_model_set_path(amusd_model* m, int path);
 /* The decode forward (AMUSD_PATH_DECODE) streams its own weight layout: 16-row x 512-K
  * units, 16-byte chunks swizzled for ldmatrix.  amusd_decode_bytes = its size (0: shapes not
  * supported); amusd_model_set_decode tiles the row-major weights into the caller's buffer
  * (the library never allocates), buf = NULL detaches it. */
 size_t amusd_decode_bytes(amusd_model* m);
+/* The cluster decode forward's weight layout (per layer: QKV / O by KV group, gate/up and
+ * down^T by 16-feature block); same contract as amusd_decode_bytes / amusd_model_set_decode. */
+size_t amusd_cluster_bytes(amusd_model* m);
+int amusd_model_set_cluster(amusd_model* m, void* buf, size_t bytes);
 int amusd_model_set_decode(amusd_model* m, void* buf, size_t bytes);
 /* Drop the caller's row-major layer weights from the model (the persistent path
  * reads only its tile-contiguous copy): afterwards the caller may free them

@@ -37,7 +37,7 @@ class TfWeights(C.Structure):
         (n, C.c_void_p * MAX_LAYERS) for n in ("attn_norm", "wqkv", "wo", "mlp_norm", "wgate", "wup", "wdown")]
 
 
-PATH_PERSISTENT, PATH_KERNELS, PATH_SIMT, PATH_DECODE = 0, 1, 2, 3  # amusd_model_set_path
+PATH_PERSISTENT, PATH_KERNELS, PATH_SIMT, PATH_DECODE, PATH_CLUSTER = 0, 1, 2, 3, 4  # amusd_model_set_path
 
 
 class SessionDesc(C.Structure):
@@ -88,6 +88,8 @@ SIGNATURES = [
     ("amusd_peer_enable", _I, [_I, _I]),
     ("amusd_prefill_bytes", _SZ, [_VP, _I]),
     ("amusd_decode_bytes", _SZ, [_VP]),
+    ("amusd_cluster_bytes", _SZ, [_VP]),
+    ("amusd_model_set_cluster", _I, [_VP, _VP, _SZ]),
     ("amusd_model_set_decode", _I, [_VP, _VP, _SZ]),
     ("amusd_model_set_prefill", _I, [_VP, _VP, _SZ, _I]),
     ("amusd_session_tp_inbox", _I, [_VP, _P(_VP)]),

@@ -9,7 +9,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libamusd.so"
-SOURCES = ["api.cu", "protocol.cu", "transformer.cu", "gemm_tc.cu", "forward_tc.cu", "prefill.cu", "decode_gv.cu"]
+SOURCES = ["api.cu", "protocol.cu", "transformer.cu", "gemm_tc.cu", "forward_tc.cu", "prefill.cu", "decode_gv.cu", "decode_cl.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

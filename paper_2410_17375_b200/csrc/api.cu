@@ -15,6 +15,7 @@
 
 #include "../../include/amusd.h"
 #include "common.cuh"
+#include "decode_cl.h"
 #include "decode_gv.h"
 #include "internal.h"
 #include "protocol.h"
@@ -132,6 +133,12 @@ struct amusd_model {
   // persistent SIMT decode forward (decode_gv.cu, AMUSD_PATH_DECODE): counters, per-CTA sums
   // of squares, attention split partials
   bool gv_ok = false;
+  // cluster decode forward (decode_cl.cu, AMUSD_PATH_CLUSTER)
+  bool cl_ok = false;
+  const uint8_t* cl_wt = nullptr;  // cluster-decode weight layout (amusd_model_set_cluster, caller-owned)
+  float* cl_h = nullptr;
+  unsigned long long* cl_acc = nullptr;
+  int* cl_sync = nullptr;
   const uint8_t* gv_wt = nullptr;  // decode-layout weights (amusd_model_set_decode, caller-owned)
   int* gv_sync = nullptr;
   float* gv_ss = nullptr;
@@ -266,6 +273,15 @@ static size_t tf_carve(const amusd_tf_config* c, void* base, amusd_model* m, con
     fattn_ws = cv.take<float>((size_t)c->n_kv_heads * KMAX * fw::attn_splits(c->max_seq) * group * (c->head_dim + 2));
     fattn_cnt = cv.take<int>((size_t)c->n_kv_heads * KMAX * fw::kCounterInts);
   }
+  const bool clok = tc && cl::supported(c->d_model, c->n_heads, c->n_kv_heads, c->head_dim, c->ffn, c->vocab);
+  float* clh = nullptr;
+  unsigned long long* clacc = nullptr;
+  int* clsync = nullptr;
+  if (clok) {
+    clh = cv.take<float>(cl::h_bytes(c->d_model) / 4);
+    clacc = cv.take<unsigned long long>(cl::acc_bytes(c->d_model) / 8);
+    clsync = cv.take<int>(cl::sync_ints());
+  }
   const bool gvok = tc && gv::supported(c->d_model, c->n_heads, c->n_kv_heads, c->head_dim, c->ffn, c->vocab);
   int* gsync = nullptr;
   float *gss = nullptr, *gattn = nullptr;
@@ -287,6 +303,7 @@ static size_t tf_carve(const amusd_tf_config* c, void* base, amusd_model* m, con
       m->fw_attn_cnt_ints = (size_t)c->n_kv_heads * KMAX * fw::kCounterInts;
     }
     m->gv_ok = gvok; m->gv_sync = gsync; m->gv_ss = gss; m->gv_attn_ws = gattn;
+    m->cl_ok = clok; m->cl_h = clh; m->cl_acc = clacc; m->cl_sync = clsync;
     m->fw_xb = fxb; m->fw_sspb = fsspb; m->fw_tflag = ftflag; m->fw_agrp = fagrp;
     m->tc = tc; m->xa_b = xa_b; m->attn_b = attn_b; m->act_b = act_b; m->inv = inv; m->ssp = ssp_b; m->tc_ws = ws; m->tc_cnt = cnt; m->tiled = tiled;
     m->seq = seq; m->tok = tok; m->api_ctl = ctl; m->kc = kc; m->vc = vc; m->h = h; m->qkv = qkv;
@@ -438,8 +455,14 @@ static bool use_fw(const amusd_model* m) {
 static bool use_gv(const amusd_model* m) {
   return m->kind == 0 && m->gv_ok && m->gv_wt && m->path == AMUSD_PATH_DECODE;
 }
-// A persistent forward (tcgen05 work queue or SIMT decode): one launch, grid from fw_grid.
-static bool use_persistent(const amusd_model* m) { return use_fw(m) || use_gv(m); }
+// Cluster decode forward (decode_cl.cu): the draft's path (AMUSD_PATH_CLUSTER).
+static bool use_cl(const amusd_model* m) {
+  return m->kind == 0 && m->cl_ok && m->cl_wt && m->path == AMUSD_PATH_CLUSTER;
+}
+// A persistent forward (tcgen05 work queue, decode or cluster decode): one launch, grid from fw_grid.
+static bool use_persistent(const amusd_model* m) { return use_fw(m) || use_gv(m) || use_cl(m); }
+// Rows one forward of this model can carry (host-driven API forwards are chunked to it).
+static int max_rows(const amusd_model* m) { return use_cl(m) ? cl::kMaxRows : KMAX; }
 // Per-kernel tcgen05 path for 16-row forwards (2-row draft steps take the SIMT GEMVs).
 static bool use_tc(const amusd_model* m, int nr) {
   return m->kind == 0 && m->tc && nr > 2 && m->path != AMUSD_PATH_SIMT;
@@ -519,6 +542,37 @@ static int gv_forward(amusd_model* m, StepCtl* ctl, cudaStream_t st, bool want_l
   return AMUSD_OK;
 }
 
+// The whole forward as one cluster-decode launch (decode_cl.cu).
+static int cl_forward(amusd_model* m, StepCtl* ctl, cudaStream_t st, bool want_logits) {
+  const amusd_tf_config& c = m->cfg;
+  cl::ClArgs a;
+  std::memset(&a, 0, sizeof(a));
+  const cl::Layout t = cl::layout(c.d_model, c.n_heads, c.n_kv_heads, c.head_dim, c.ffn, c.vocab, c.n_layers);
+  a.wt = m->cl_wt; a.layer_bytes = t.layer_bytes; a.off_o = t.off_o; a.off_gu = t.off_gu; a.off_dn = t.off_dn;
+  a.wt_lm = m->cl_wt + t.lm_off;
+  a.embed = (const __nv_bfloat16*)m->w.embed;
+  a.norms = m->fw_norms;
+  a.cos = m->w.rope_cos; a.sin = m->w.rope_sin;
+  a.ctl = ctl;
+  a.kcache = (char*)m->kc; a.vcache = (char*)m->vc; a.kv_layer_bytes = (long long)m->kv_layer_elems * 2;
+  a.h = m->cl_h; a.acc = m->cl_acc; a.sync = m->cl_sync; a.best = m->fw_best;
+  a.logits = want_logits ? m->logits : nullptr;
+  a.ab_req = m->fw_ab_req; a.ab_done = m->fw_ab_done;
+  a.cuts = m->fw_sched ? fw::cut_counter(m->fw_sched) : nullptr;
+  a.d = c.d_model; a.H = c.n_heads; a.KV = c.n_kv_heads; a.hd = c.head_dim; a.ffn = c.ffn; a.vocab = c.vocab;
+  a.L = c.n_layers; a.S = c.max_seq; a.eos = c.eos_token; a.exclude_eos = c.exclude_eos;
+  a.eps = c.norm_eps; a.scale = 1.0f / sqrtf((float)c.head_dim);
+  a.stages = std::max(2, std::min(cl::max_stages(c.d_model, c.n_heads, c.n_kv_heads, c.head_dim),
+                                  env_int("AMUSD_CL_STAGES", 99)));
+  a.debug = env_int("AMUSD_GV_DEBUG", 0);
+  a.l2_ahead = env_int("AMUSD_CL_L2", 0);
+  const int grid = cl::grid_for(a, m->fw_grid > 0 ? m->fw_grid : model_sms(m));
+  if (m->fw_dbg && (size_t)m->fw_dbg_items * 8 >= (size_t)grid * cl::kDbgPerLayer * c.n_layers) a.dbg = m->fw_dbg;
+  if (grid <= 0) return fail(AMUSD_ERR_UNSUPPORTED, "cluster decode: too few SMs for one 8-CTA cluster per KV head");
+  CUDA_TRY(cl::launch(a, grid, st));
+  return AMUSD_OK;
+}
+
 // Enqueue one forward of `m` driven by control block `ctl` (rows <= nr).
 static int model_forward(amusd_model* m, StepCtl* ctl, int nr, cudaStream_t st, bool pdl, bool want_logits) {
   if (m->kind == 1) {
@@ -526,6 +580,10 @@ static int model_forward(amusd_model* m, StepCtl* ctl, int nr, cudaStream_t st, 
                                  m->agree_thr, m->script, m->script_len, m->eos_position, st));
     return AMUSD_OK;
   }
+  // co-located AMUSD draft (fw_part_ok): the cluster kernel's grid barrier needs every cluster
+  // resident, which the verify forward beside it does not guarantee -> the work-queue forward
+  if (use_cl(m) && !m->fw_part_ok) return cl_forward(m, ctl, st, want_logits);
+  if (use_cl(m) && m->fw_ready) return fw_forward(m, ctl, st, want_logits);
   if (use_gv(m)) return gv_forward(m, ctl, st, want_logits);
   if (use_fw(m)) return fw_forward(m, ctl, st, want_logits);
   if (!m->row_major) return fail(AMUSD_ERR_UNSUPPORTED, "row-major weights released: persistent path only");
@@ -816,7 +874,12 @@ int amusd_model_set_timeline(amusd_model* m, void* buf, size_t bytes) {
 
 int amusd_model_set_path(amusd_model* m, int path) {
   if (!m) return fail(AMUSD_ERR_INVALID_INPUT, "null model");
-  if (path < AMUSD_PATH_PERSISTENT || path > AMUSD_PATH_DECODE) return fail(AMUSD_ERR_INVALID_INPUT, "unknown path");
+  if (path < AMUSD_PATH_PERSISTENT || path > AMUSD_PATH_CLUSTER) return fail(AMUSD_ERR_INVALID_INPUT, "unknown path");
+  if (path == AMUSD_PATH_CLUSTER && (m->kind != 0 || !m->cl_ok))
+    return fail(AMUSD_ERR_UNSUPPORTED, "the cluster decode forward needs a bf16 model with d_model <= 2048 (64-multiple), "
+                                       "16-row output blocks, head_dim 64/128 and <= 8 query heads per KV head");
+  if (path == AMUSD_PATH_CLUSTER && !m->cl_wt)
+    return fail(AMUSD_ERR_INVALID_INPUT, "attach the cluster decode weight layout first (amusd_model_set_cluster)");
   if (path == AMUSD_PATH_DECODE && (m->kind != 0 || !m->gv_ok))
     return fail(AMUSD_ERR_UNSUPPORTED, "the decode forward needs a bf16 model with 64-multiple GEMV widths, 16-row "
                                        "output blocks, head_dim 64/128 and <= 8 query heads per KV head");
@@ -827,6 +890,34 @@ int amusd_model_set_path(amusd_model* m, int path) {
   if (m->kind == 0 && path != AMUSD_PATH_PERSISTENT && !m->row_major)
     return fail(AMUSD_ERR_UNSUPPORTED, "the row-major weights were released: only the persistent path remains");
   m->path = path;
+  return AMUSD_OK;
+}
+
+size_t amusd_cluster_bytes(amusd_model* m) {
+  if (!m || m->kind != 0 || !m->cl_ok) return 0;
+  const amusd_tf_config& c = m->cfg;
+  return (size_t)cl::layout(c.d_model, c.n_heads, c.n_kv_heads, c.head_dim, c.ffn, c.vocab, c.n_layers).total;
+}
+
+int amusd_model_set_cluster(amusd_model* m, void* buf, size_t bytes) {
+  if (!m) return fail(AMUSD_ERR_INVALID_INPUT, "null model");
+  if (!buf) {
+    if (m->path == AMUSD_PATH_CLUSTER) return fail(AMUSD_ERR_INVALID_INPUT, "the cluster decode path is selected");
+    m->cl_wt = nullptr;
+    return AMUSD_OK;
+  }
+  if (m->kind != 0 || !m->cl_ok) return fail(AMUSD_ERR_UNSUPPORTED, "this model's shapes do not take the cluster decode");
+  if (!m->row_major) return fail(AMUSD_ERR_UNSUPPORTED, "the row-major weights were released");
+  if (bytes < amusd_cluster_bytes(m)) return fail(AMUSD_ERR_INVALID_INPUT, "cluster decode weight buffer too small");
+  const amusd_tf_config& c = m->cfg;
+  const cl::Layout t = cl::layout(c.d_model, c.n_heads, c.n_kv_heads, c.head_dim, c.ffn, c.vocab, c.n_layers);
+  uint8_t* dst = (uint8_t*)buf;
+  for (int l = 0; l < c.n_layers; ++l)
+    CUDA_TRY(cl::tile_layer(m->w.wqkv[l], m->w.wo[l], m->w.wgate[l], m->w.wup[l], m->w.wdown[l], c.d_model, c.n_heads,
+                            c.n_kv_heads, c.head_dim, c.ffn, dst + (size_t)l * t.layer_bytes, 0));
+  CUDA_TRY(cl::tile_lm(m->w.lm_head, c.vocab, c.d_model, dst + t.lm_off, 0));
+  CUDA_TRY(cudaDeviceSynchronize());
+  m->cl_wt = dst;
   return AMUSD_OK;
 }
 
@@ -1009,13 +1100,13 @@ static int prefill_min_tokens() {
 static int catch_up(amusd_model* m, int keep, cudaStream_t st) {
   if (m->kv_len >= m->len) m->kv_len = m->len - 1;
   const int todo = m->len - keep - m->kv_len;
-  if (m->pf_ready && m->kv_len == 0 && m->tp.tp_size < 2 && use_fw(m) && todo >= prefill_min_tokens() &&
+  if (m->pf_ready && m->kv_len == 0 && m->tp.tp_size < 2 && m->tc && m->fw_ready && todo >= prefill_min_tokens() &&
       todo <= m->pf.max_tokens) {
     if (int r = prefill_forward(m, todo, st)) return r;
     m->kv_len = todo;
   }
   while (m->len - m->kv_len > keep) {
-    const int rows = std::min(KMAX, m->len - m->kv_len - keep);
+    const int rows = std::min(max_rows(m), m->len - m->kv_len - keep);
     int r = api_forward(m, m->kv_len, m->htok.data() + m->kv_len, rows, nullptr, st);
     if (r) return r;
     m->kv_len += rows;
@@ -1058,7 +1149,7 @@ int amusd_next_token(amusd_model* m, int32_t* out, void* stream) {
   if (!m || !out) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
   if (int r = sync_from_device(m, st)) return r;
   if (m->pred_valid) { *out = m->pred; return AMUSD_OK; }
-  if (int r = catch_up(m, KMAX, st)) return r;
+  if (int r = catch_up(m, max_rows(m), st)) return r;
   const int rows = m->len - m->kv_len;
   int preds[KMAX];
   if (int r = api_forward(m, m->kv_len, m->htok.data() + m->kv_len, rows, preds, st)) return r;
@@ -1121,7 +1212,7 @@ int amusd_verify_tokens(amusd_model* m, const int32_t* cands, int n, int32_t* pr
   int pos = m->kv_len, done = 0;
   int buf[KMAX];
   while (done < (int)rows_tok.size()) {
-    const int rows = std::min(KMAX, (int)rows_tok.size() - done);
+    const int rows = std::min(max_rows(m), (int)rows_tok.size() - done);
     if (int r = api_forward(m, pos, rows_tok.data() + done, rows, buf, st)) return r;
     for (int i = 0; i < rows; ++i) preds[done + i] = buf[i];
     done += rows;

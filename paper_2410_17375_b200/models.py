@@ -447,7 +447,7 @@ class TransformerModel(CudaModel):
         return {n: self._synthetic_one(i, n, tdt, seed, std) for i, n in enumerate(weight_names(self.config))}
 
     PATHS = {"persistent": L.PATH_PERSISTENT, "kernels": L.PATH_KERNELS, "simt": L.PATH_SIMT,
-             "decode": L.PATH_DECODE}
+             "decode": L.PATH_DECODE, "cluster": L.PATH_CLUSTER}
 
     def set_path(self, path: str) -> None:
         """Select the forward implementation: 'persistent' (one tcgen05 launch per forward,
@@ -464,13 +464,21 @@ class TransformerModel(CudaModel):
             with torch.cuda.device(self.device):
                 L.check(self._lib.amusd_model_set_decode(self._h, C.c_void_p(buf.data_ptr()), nbytes))
             self._decode_w = buf   # decode-layout weights (~ the model's weight bytes), owned here
+        if path == "cluster" and getattr(self, "_cluster_w", None) is None:
+            nbytes = self._lib.amusd_cluster_bytes(self._h)
+            if nbytes == 0:
+                raise InvalidInputError("this model's shapes do not take the cluster decode forward")
+            buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            with torch.cuda.device(self.device):
+                L.check(self._lib.amusd_model_set_cluster(self._h, C.c_void_p(buf.data_ptr()), nbytes))
+            self._cluster_w = buf
         L.check(self._lib.amusd_model_set_path(self._h, self.PATHS[path]))
         self.path = path
 
     def kernels_per_forward(self) -> int:
         c = self.config
         tc = c.dtype == "bf16" and c.use_tensor_cores
-        if tc and getattr(self, "path", "persistent") in ("persistent", "decode"):
+        if tc and getattr(self, "path", "persistent") in ("persistent", "decode", "cluster"):
             return 1
         return 1 + 5 * c.n_layers + 2
 

@@ -35,13 +35,17 @@ def _rel(x, ref):
     return float(np.abs(x - ref).max() / ref.std())
 
 
+PATHS = ["decode", "cluster"]
+
+
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("shape,layers", [("tiny_draft", None), ("tiny_verify", None), ("llama_1b", 2)])
-def test_decode_logits_vs_oracle(shape, layers):
+def test_decode_logits_vs_oracle(shape, layers, path):
     TC = P.TransformerConfig
     kw = dict(dtype="bf16", max_seq=320) if shape.startswith("tiny") else dict(max_seq=320, n_layers=layers)
     cfg = getattr(TC, shape)(**kw)
     m = P.TransformerModel(cfg, seed=5)
-    m.set_path("decode")
+    m.set_path(path)
     rf = RefDecoder(shape_of(cfg, kv_bf16=True, act_bf16=True), m.host_weights(), tied=cfg.tied)
     prompt = (PROMPT * 12)[:150]          # crosses the 128-position attention split
     st = m.init_state(prompt)
@@ -49,7 +53,7 @@ def test_decode_logits_vs_oracle(shape, layers):
     gl = m.last_logits(1).numpy()[0]
     rs = rf.start(prompt)
     err = _rel(gl, rs.last_logits)
-    print(f"{shape}: decode path max|gpu-cpu|/std {err:.3e}")
+    print(f"{shape}: {path} path max|gpu-cpu|/std {err:.3e}")
     assert err < TOL, err
     # window of 6 rows (> 4: the multi-group path) vs the oracle's verify
     cands = [101, 202, 303, 404, 505, 606]
@@ -66,13 +70,14 @@ def test_decode_logits_vs_oracle(shape, layers):
     P.engines.clear_sessions()
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("plen", [40, 126, 250])
-def test_decode_rows_invariant(plen):
+def test_decode_rows_invariant(plen, path):
     """Logits of a row do not depend on the rows sharing the forward (1..7: single- and
     multi-group paths) nor on window vs incremental forwards."""
     TC = P.TransformerConfig
     m = P.TransformerModel(TC.llama_1b(max_seq=352, n_layers=3), seed=32)
-    m.set_path("decode")
+    m.set_path(path)
     prompt = (PROMPT * 12)[:plen]
     cands = [101, 202, 303, 404, 505, 606, 707]
     m.verify_tokens(m.init_state(prompt), cands)
@@ -92,7 +97,8 @@ def test_decode_rows_invariant(plen):
     P.engines.clear_sessions()
 
 
-def test_decode_full_depth_1b_vs_oracle():
+@pytest.mark.parametrize("path", PATHS)
+def test_decode_full_depth_1b_vs_oracle(path):
     """Full-depth Llama-3.2-1B shape (the bench draft) vs the bf16-faithful oracle."""
     import torch
     try:
@@ -104,7 +110,7 @@ def test_decode_full_depth_1b_vs_oracle():
     TC = P.TransformerConfig
     cfg = TC.llama_1b(max_seq=96)
     m = P.TransformerModel(cfg, seed=1)
-    m.set_path("decode")
+    m.set_path(path)
     w = m.host_weights()
     prompt = PROMPT + PROMPT[:8]
     st = m.init_state(prompt)
@@ -115,7 +121,7 @@ def test_decode_full_depth_1b_vs_oracle():
     r64 = RefDecoder(shape_of(cfg, kv_bf16=True, act_bf16=True, acc64=True), w, tied=cfg.tied)
     floor = _rel(r64.start(prompt).last_logits, ref)
     err = _rel(gl, ref)
-    print(f"llama_1b decode path: max|gpu-cpu|/std {err:.3e} (fp32 noise floor {floor:.3e}); "
+    print(f"llama_1b {path} path: max|gpu-cpu|/std {err:.3e} (fp32 noise floor {floor:.3e}); "
           f"argmax gpu {int(np.argmax(gl))} cpu {int(np.argmax(ref))}")
     assert err <= max(2.0 * floor, 1e-2), (err, floor)
     del m, w, rf, r64
@@ -123,13 +129,14 @@ def test_decode_full_depth_1b_vs_oracle():
     torch.cuda.empty_cache()
 
 
-def test_engines_with_decode_draft(monkeypatch):
+@pytest.mark.parametrize("path", PATHS)
+def test_engines_with_decode_draft(monkeypatch, path):
     """AMUSD (co-located, draft cut on) and sync-SD with a decode-path draft: tokens == AR,
     valid traces; the cut fires; the draft's own greedy decode is unchanged afterwards."""
     TC = P.TransformerConfig
     v = P.TransformerModel(TC.tiny_verify(dtype="bf16", max_seq=320), seed=3)
     d = P.TransformerModel(TC.tiny_draft(dtype="bf16", max_seq=320), seed=4)
-    d.set_path("decode")
+    d.set_path(path)
     cfg = P.DecodeConfig(max_new_tokens=96)
     ar = P.decode_autoregressive(v, PROMPT, cfg)
     d_ar = P.decode_autoregressive(d, PROMPT, cfg).tokens
