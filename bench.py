@@ -318,7 +318,9 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
         vcfg, dcfg = TC.tiny_verify(max_seq=max_seq), TC.tiny_draft(max_seq=max_seq)
     else:
         vcfg, dcfg = TC.llama_8b(max_seq=max_seq), TC.llama_1b(max_seq=max_seq)
-    vm = P.TransformerModel(vcfg, seed=0, device=dev)
+    # the verify keeps only its tcgen05 copy (the row-major one would be 16 GB more for the 8B);
+    # the draft keeps both (the roofline block also tiles it for the decode forward)
+    vm = P.TransformerModel(vcfg, seed=0, device=dev, keep_row_major=args.shapes == "tiny")
     dm = P.TransformerModel(dcfg, seed=1, device=dev)
     prompt = synthetic_prompt(Plen, vcfg.vocab_size)
     draft = P.AgreementDraft(dm, args.rho, coin_seed=1234)
