@@ -583,8 +583,8 @@ static int model_forward(amusd_model* m, StepCtl* ctl, int nr, cudaStream_t st, 
   // co-located AMUSD draft (fw_part_ok): the cluster kernel's grid barrier needs every cluster
   // resident, which the verify forward beside it does not guarantee -> the work-queue forward
   if (use_cl(m) && !m->fw_part_ok) return cl_forward(m, ctl, st, want_logits);
-  if (use_cl(m) && m->fw_ready) return fw_forward(m, ctl, st, want_logits);
-  if (use_gv(m)) return gv_forward(m, ctl, st, want_logits);
+  if (use_gv(m) && !m->fw_part_ok) return gv_forward(m, ctl, st, want_logits);
+  if ((use_cl(m) || use_gv(m)) && m->fw_ready) return fw_forward(m, ctl, st, want_logits);
   if (use_fw(m)) return fw_forward(m, ctl, st, want_logits);
   if (!m->row_major) return fail(AMUSD_ERR_UNSUPPORTED, "row-major weights released: persistent path only");
   if (use_tc(m, nr)) {
