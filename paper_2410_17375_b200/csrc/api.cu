@@ -1647,8 +1647,9 @@ int amusd_session_kernels_per_step(amusd_session* s, int engine, int* draft_step
   if (!s || !draft_step || !verify_step) return fail(AMUSD_ERR_INVALID_INPUT, "null argument");
   *draft_step = s->draft ? model_kernels_per_forward(s->draft, 2) + 2 : 0;
   // the AMUSD draft's persistent forward is followed by the cut cleanup (a no-op launch when not cut)
-  if ((engine == AMUSD_ENGINE_ASYNC || engine == AMUSD_ENGINE_ASYNC_DRAFT) && s->draft && use_fw(s->draft) &&
-      env_int("AMUSD_FW_CUT", 1))
+  // (co-located AMUSD runs a decode-path draft on the work-queue forward too, see model_forward)
+  const bool wq = s->draft && (use_fw(s->draft) || (engine == AMUSD_ENGINE_ASYNC && use_persistent(s->draft)));
+  if ((engine == AMUSD_ENGINE_ASYNC || engine == AMUSD_ENGINE_ASYNC_DRAFT) && wq && env_int("AMUSD_FW_CUT", 1))
     *draft_step += 1;
   *verify_step = s->verify ? model_kernels_per_forward(s->verify, KMAX) + 2 : 0;
   if (engine == AMUSD_ENGINE_SYNC) *verify_step += 1;
