@@ -357,8 +357,16 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
         cm = ClockSampler(local_rank) if name == "amusd" else None
         if cm:
             cm.__enter__()
+        pre_ms = []
         for _ in range(args.steps):
-            s.prepare(prompt)                      # prefill is reported separately (not timed)
+            # prefill is reported separately: CUDA events on the verify stream it runs on
+            vs_ = s.streams()[0]
+            p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            p0.record(vs_)
+            s.prepare(prompt)
+            p1.record(vs_)
+            p1.synchronize()
+            pre_ms.append(p0.elapsed_time(p1))
             start, end = s.launch(eng)
             out = s.collect(start, end)
             tokens, _ = finalize_tokens(out.verified, vm.eos_token, N)
@@ -390,6 +398,7 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
             "verify_steps": statistics.mean(i.verify_steps for i in stats),
             "rollbacks": statistics.mean(i.rollbacks for i in stats),
             "drafted": statistics.mean(i.drafted for i in stats),
+            "prefill_ms": round(max(pre_ms), 3),   # both models' prefill (init_state), not in ms_per_step
         }
         # in-situ HBM bandwidth of the run: forwards issued x their algorithmic bytes over the
         # device time (AMUSD: every draft forward launched, cut ones counted in full -> upper bound)
