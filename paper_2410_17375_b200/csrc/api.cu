@@ -169,6 +169,9 @@ static int fw_units() {
   if (v < 0) v = std::max(1, env_int("AMUSD_FW_UNITS", 16));
   return v;
 }
+// AMUSD_FW_FUSE: gate/up -> down fused in the persistent forward where the shape allows it
+// (read when a model is created; forward_tc.h FwArgs::fuse).
+static int fw_fuse() { return env_int("AMUSD_FW_FUSE", 0); }
 static int num_sms() { return device_sms(); }
 // SMs of this model's persistent launches outside co-located AMUSD (amusd_model_set_max_grid).
 static int model_sms(const amusd_model* m) { return m->max_grid > 0 ? std::min(m->max_grid, num_sms()) : num_sms(); }
@@ -201,6 +204,7 @@ static bool fw_sizes(const amusd_tf_config* c, const amusd_tp_shard* sh, size_t*
   fw::ModelView v{};
   v.d = c->d_model; v.H = c->n_heads; v.KV = c->n_kv_heads; v.hd = c->head_dim; v.ffn = c->ffn; v.vocab = c->vocab;
   v.L = c->n_layers; v.S = c->max_seq;
+  v.fuse = fw_fuse();
   view_shard(&v, sh);
   fw::FwArgs a{};
   return fw::build_kinds(v, fw_units(), &a, ws_floats, cnt_ints, max_tiles);
@@ -699,6 +703,7 @@ static int tf_create(amusd_model** out, const amusd_tf_config* cfg, const amusd_
       fw::ModelView v{};
       v.d = d; v.H = c.n_heads; v.KV = c.n_kv_heads; v.hd = c.head_dim; v.ffn = c.ffn; v.vocab = c.vocab;
       v.L = c.n_layers; v.S = c.max_seq;
+      v.fuse = fw_fuse();
       v.wt_layer0 = m->wt_qkv[0];
       v.wt_layer_bytes = c.n_layers > 1 ? (long long)(m->wt_qkv[1] - m->wt_qkv[0]) : 0;
       v.wt_lm = m->wt_lm; v.norms = m->fw_norms;

@@ -226,6 +226,8 @@ AMUSD_DEV int gemm_of(int kind) {
   return kind == kKQkv ? kGQkv : kind == kKO ? kGO : kind == kKGu ? kGGu : kind == kKDown ? kGDown : kGLm;
 }
 AMUSD_DEV bool is_gemm(int kind) { return kind != kKAttn && kind != kKEmbed; }
+// Per-tile (fine) dependencies for consumer `kind` (AMUSD_FW_FINE bit 1 << kind).
+AMUSD_DEV bool fine_for(const FwArgs& a, int kind) { return (a.fine >> kind) & 1; }
 
 // item index -> (phase, index within the phase)
 AMUSD_DEV int2 locate(const FwArgs& a, const Lay& L, int i) {
@@ -814,7 +816,7 @@ constexpr int epi_bytes() { return ((int)sizeof(EpiSmem) + 127) & ~127; }
 // TP: a tensor-parallel shard's instance (cross-rank split-K reduce, all-rank argmax).  The
 // unsharded instance compiles those branches out: as runtime checks in the split-K path they
 // cost 8% (8B) / 17% (1B) of the forward.
-template <int HD, int G, int MINB, bool TP>
+template <int HD, int G, int MINB, bool TP, bool FUSE>
 __global__ void __launch_bounds__(kThreads, MINB)
     k_forward(const __grid_constant__ CUtensorMap m_xa, const __grid_constant__ CUtensorMap m_attn,
               const __grid_constant__ CUtensorMap m_act, const __grid_constant__ CUtensorMap m_xb,
@@ -840,6 +842,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
   int* s_lay = (int*)(tmem_slot + 1);  // A, rows, pos0, active, epoch
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // FUSE: [0] act tile written (epilogue -> X loader), [1] down-slab MMAs done (MMA -> epilogue),
+  // [2] down-slab accumulators free (epilogue -> MMA)
+  __shared__ uint64_t s_fb[3];
+  constexpr uint32_t kCols = FUSE ? 512 : kTmemCols;  // FUSE: 16 down-slab accumulators after the 256
   if (threadIdx.x == 0) {
     const StepCtl* c = a.ctl;
     const int active = c->active;
@@ -859,6 +865,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
     for (int i = 0; i < kTbuf; ++i) { mbar_init(smem_u32(&tfull[i]), NACC); mbar_init(smem_u32(&tempty[i]), 128); }
     for (int i = 0; i < kQ; ++i) { mbar_init(smem_u32(&qfull[i]), 1); mbar_init(smem_u32(&qempty[i]), 1 + NACC + 1); }
     mbar_init(smem_u32(&((AttnSmem<HD, G>*)scratch)->bar), 1);
+    if (FUSE) {
+      mbar_init(smem_u32(&s_fb[0]), 1);
+      mbar_init(smem_u32(&s_fb[1]), NACC);
+      mbar_init(smem_u32(&s_fb[2]), 128);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -882,7 +893,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
   const Lay& L = s_L;
   if (warp == kWarpMma0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(kTmemCols));
+                 "n"(kCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -974,7 +985,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
             prefetch_l2(a.g[kGQkv].wt + (size_t)(layer_of(pj.x) + 1) * a.g[kGQkv].wt_stride + lo, (uint32_t)(hi - lo),
                         pol_keep);
         }
-        if (is_gemm(kind)) {
+        if (is_gemm(kind) && !(FUSE && kind == kKDown)) {  // (FUSE: down items carry no weights)
           const GemmRes g = resolve(a, gemm_of(kind), layer_of(pj.x));
           const int c = pj.y / g.ntiles, t = pj.y - c * g.ntiles;  // chunk-major item order
           const uint8_t* src = g.wt + ((size_t)t * g.kb + (size_t)c * g.kc) * kWBytes;
@@ -1001,6 +1012,29 @@ __global__ void __launch_bounds__(kThreads, MINB)
                 bulk_load(dst, from, kWBytes, smem_u32(&wfull[s]), pol_w);
             }
           }
+          if (FUSE && kind == kKGu && c == g.nchunks - 1) {
+            // the tile's merging chunk: the down weights of its 64 features, unit (output tile o,
+            // K unit t) of every output tile (the down layout is tile-major, 64-wide K units)
+            const GemmRes gd = resolve(a, kGDown, layer_of(pj.x));
+            const int nt = a.g[kGDown].ntiles;
+            for (int o = 0; o < nt; o += kUPS, ++gu, rg.next(S)) {
+              const int s = rg.s;
+              mbar_wait_t(smem_u32(&empty[s]), rg.ph ^ 1u);
+              if (inflight < S && gu >= inflight) {
+                mbar_wait_t(smem_u32(&wfull[rl.s]), rl.ph);
+                rl.next(S);
+              }
+              if (a.debug & 8) {
+                mbar_arrive(smem_u32(&wfull[s]));
+                continue;
+              }
+              mbar_expect_tx(smem_u32(&wfull[s]), kStageW);
+#pragma unroll
+              for (int uu = 0; uu < kUPS; ++uu)
+                bulk_load(smem_u32(sW + s * kStageW + uu * kWBytes), gd.wt + ((size_t)(o + uu) * gd.kb + t) * kWBytes,
+                          kWBytes, smem_u32(&wfull[s]), pol_w);
+            }
+          }
           dbg_mark(a, i, 2, globaltimer());
         }
         if (!have_next) {  // peek; an attention item waits until this CTA's pipeline has drained
@@ -1018,7 +1052,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     // ===== activation loader: dependency wait, then X tiles by TMA =====
     if (lane == 0) {
       const uint64_t pol_x = policy_evict_last();  // X is re-read by every CTA of the phase
-      int n = 0, dep_ok = -1;
+      int n = 0, dep_ok = -1, fz = 0;
       Ring rg;
       for (;;) {
         const int slot = n % kQ;
@@ -1028,7 +1062,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         ++n;
         if (it.x < 0) break;
         const int kind = kind_of(it.x, a.L);
-        if (!is_gemm(kind)) continue;
+        if (!is_gemm(kind) || (FUSE && kind == kKDown)) continue;
         const GemmKind& g = a.g[gemm_of(kind)];
         const int c = it.y / g.ntiles, kc = g.kc, layer = layer_of(it.x);
         const int prod = it.x - 1;  // producer phase
@@ -1036,7 +1070,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           // Fine-grained: wait only for the producer tiles covering this item's K range --
           // unless the whole producer phase is already known (or now seen) complete.
           const int k0 = c * kc * BK, k1 = k0 + kc * BK;  // input columns [k0, k1)
-          if (!a.fine) {  // phase-level dependency (default, measured faster)
+          if (!fine_for(a, kind)) {  // phase-level dependency (default, measured faster)
             wait_count(done + prod * kPad, phase_count(a, L, prod));
             dep_ok = prod;
           } else if (ld_acquire_gpu(done + prod * kPad) >= phase_count(a, L, prod)) {
@@ -1071,13 +1105,28 @@ __global__ void __launch_bounds__(kThreads, MINB)
             tma_load_2d(smem_u32(sX + s * kStageX + uu * kXBytes), map, (c * kc + u + uu) * BK, 0,
                         smem_u32(&xfull[s]), pol_x);
         }
+        if (FUSE && kind == kKGu && c == g.nchunks - 1) {  // the act tile of these 64 features, once written
+          mbar_wait_t(smem_u32(&s_fb[0]), fz & 1);
+          ++fz;
+          fence_proxy_async();
+          const int nt = a.g[kGDown].ntiles;
+          for (int o = 0; o < nt; o += kUPS, rg.next(S)) {
+            const int s = rg.s;
+            mbar_wait_t(smem_u32(&empty[s]), rg.ph ^ 1u);
+            mbar_expect_tx(smem_u32(&xfull[s]), kStageX);
+#pragma unroll
+            for (int uu = 0; uu < kUPS; ++uu)
+              tma_load_2d(smem_u32(sX + s * kStageX + uu * kXBytes), &m_act, (it.y - c * g.ntiles) * BK, 0,
+                          smem_u32(&xfull[s]), pol_x);
+          }
+        }
       }
     }
   } else if (warp < kWarpEpi0) {
     // ===== MMA issuers: warp w issues K-slice kk of every unit =====
     if (lane == 0) {
       const int kk = warp - kWarpMma0;
-      int n = 0, seg = 0;
+      int n = 0, seg = 0, fz = 0;
       Ring rg;
       for (;;) {
         const int slot = n % kQ;
@@ -1088,7 +1137,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         if (it.x < 0) break;
         const bool nomma = a.debug & 1;
         const int kind = kind_of(it.x, a.L);
-        if (!is_gemm(kind)) continue;
+        if (!is_gemm(kind) || (FUSE && kind == kKDown)) continue;
         const int kc = a.g[gemm_of(kind)].kc;
         const int b = seg % kTbuf;
         mbar_wait_t(smem_u32(&tempty[b]), ((seg / kTbuf) & 1) ^ 1);
@@ -1113,6 +1162,32 @@ __global__ void __launch_bounds__(kThreads, MINB)
         if (nomma) mbar_arrive(smem_u32(&tfull[b]));
         else umma_commit(smem_u32(&tfull[b]));
         ++seg;
+        if (FUSE && kind == kKGu && it.y / a.g[kGGu].ntiles == a.g[kGGu].nchunks - 1) {
+          // down slab (the tile's merging chunk): unit o (output tile o, K = this tile's 64 features) into its own
+          // accumulator (columns 256 + 16 o); warp kk issues the units o = kk mod 4, all 4 K16 steps
+          mbar_wait_t(smem_u32(&s_fb[2]), (fz & 1) ^ 1);
+          ++fz;
+          tc_fence_after();
+          const int nt = a.g[kGDown].ntiles;
+          for (int o = 0; o < nt; o += kUPS, rg.next(S)) {
+            const int s = rg.s;
+            const uint32_t par = rg.ph;
+            mbar_wait_t(smem_u32(&wfull[s]), par);
+            mbar_wait_t(smem_u32(&xfull[s]), par);
+            tc_fence_after();
+#pragma unroll
+            for (int uu = 0; uu < kUPS; ++uu) {
+              if (((o + uu) & (NACC - 1)) != kk || nomma) continue;
+              const uint32_t d2 = tmem + (uint32_t)(kTmemCols + (o + uu) * BN);
+#pragma unroll
+              for (int ks = 0; ks < BK / 16; ++ks)
+                umma(d2, umma_desc(smem_u32(sW + s * kStageW + uu * kWBytes) + ks * 32),
+                     umma_desc(smem_u32(sX + s * kStageX + uu * kXBytes) + ks * 32), ks > 0 ? 1u : 0u);
+            }
+            umma_commit(smem_u32(&empty[s]));
+          }
+          umma_commit(smem_u32(&s_fb[1]));
+        }
       }
     }
   } else {
@@ -1126,7 +1201,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     using AS = AttnSmem<HD, G>;
     static_assert(offsetof(AS, vb) == sizeof(((AS*)nullptr)->kb), "kb|vb contiguous");
     if (tid == 0) es->inv_phase = -1;
-    int n = 0, seg = 0, attn_dep_ok = -1;
+    int n = 0, seg = 0, attn_dep_ok = -1, ez = 0;
     uint32_t attn_par = 0;
     for (;;) {
       const int slot = n % kQ;
@@ -1139,7 +1214,35 @@ __global__ void __launch_bounds__(kThreads, MINB)
       const int p = it.x, j = it.y;
       const int kind = kind_of(p, a.L), layer = layer_of(p);
       bool wrote = true, lm_last_check = false;
-      if (is_gemm(kind)) {
+      if (FUSE && kind == kKDown) {
+        // down tile j: every gate/up tile has red.added its 64 features' partial; merge and run
+        // the residual epilogue (h, the next norm input, its sums of squares)
+        const GemmKind& g = a.g[kGDown];
+        const __nv_bfloat16* gnext = g.gnext + (size_t)layer * g.gnext_stride;
+        // Every gate/up item of THIS layer contributes to every down tile, so the dependency is
+        // the gate/up phase count (per layer; a shared per-tile counter would let a later layer's
+        // merge item, grabbed early, fire on this layer's contributions).  Nothing of the layer
+        // is read before it: h's writer, the O phase, may still be running when this is grabbed.
+        if (tid == 0) {
+          wait_count(done + (p - 1) * kPad, a.g[kGGu].nitems);
+          if (a.dbg) dbg_mark(a, phase_first(a, L, p) + j, 6, globaltimer());
+        }
+        named_bar(1, 128);
+        resid_prefetch(g, gnext, j, nl, L.rows, et);
+        cp_async_wait_all();
+        named_bar(1, 128);
+        unsigned long long* acc64 = (unsigned long long*)a.ws + (size_t)g.ws_off + (size_t)j * BN * BM + nl;
+        long long s64[BN];
+        float acc[BN];
+#pragma unroll
+        for (int r = 0; r < BN; ++r) s64[r] = r < L.rows ? (long long)__ldcg(acc64 + r * BM) : 0ll;
+#pragma unroll
+        for (int r = 0; r < BN; ++r) {
+          acc[r] = (float)((double)s64[r] * (1.0 / 4294967296.0));
+          if (r < L.rows) __stcg(acc64 + r * BM, 0ull);
+        }
+        tile_epilogue<TP>(a, g, gnext, j, nl, acc, L.rows, es, et, q, lane);
+      } else if (is_gemm(kind)) {
         const GemmKind& g = a.g[gemm_of(kind)];
         const int b = seg % kTbuf;
         mbar_wait_t(smem_u32(&tfull[b]), (seg / kTbuf) & 1);
@@ -1169,7 +1272,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         if (need_inv && final_item && es->inv_phase != p) {
           // the RMSNorm scale needs the whole input row: wait for the full producer phase
           // (the MMA above only needed the tiles of its K range)
-          if (a.fine) {  // (phase-level mode: the MMA already waited for the whole phase)
+          if (fine_for(a, kind)) {  // (phase-level mode: the MMA already waited for the whole phase)
             if (tid == 0) {
               const int prod = p - 1;  // O(l) for gate/up; down(l-1) for QKV(l); down(L-1) for the LM head
               wait_count(done + prod * kPad, phase_count(a, L, prod));
@@ -1275,6 +1378,34 @@ __global__ void __launch_bounds__(kThreads, MINB)
           const __nv_bfloat16* gnext = g.gnext ? g.gnext + (size_t)layer * g.gnext_stride : nullptr;
           tile_epilogue<TP>(a, g, gnext, t, nl, acc, L.rows, es, et, q, lane);
         }
+        if (FUSE && kind == kKGu && final) {
+          // hand the act tile (global, written above) to the X loader, then fold the down-slab
+          // products of these 64 features into the down tiles' int64 accumulators.  The TMA reads
+          // through L2: the act stores must be performed at gpu scope first (a CTA-scope hand-off
+          // alone may leave them in the SM's write path)
+          __threadfence();
+          fence_proxy_async();
+          named_bar(1, 128);
+          if (tid == 0) mbar_arrive(smem_u32(&s_fb[0]));
+          mbar_wait_t(smem_u32(&s_fb[1]), ez & 1);
+          ++ez;
+          tc_fence_after();
+          const GemmKind& gd = a.g[kGDown];
+          unsigned long long* accd = (unsigned long long*)a.ws + (size_t)gd.ws_off + nl;
+          for (int o = 0; o < gd.ntiles; ++o) {
+            float w[BN];
+            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(kTmemCols + o * BN), w);
+#pragma unroll
+            for (int r = 0; r < BN; ++r)
+              if (r < L.rows) {
+                const long long fx = __float2ll_rn(w[r] * 4294967296.0f);
+                asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(accd + (size_t)o * BN * BM + r * BM),
+                             "l"(fx) : "memory");
+              }
+          }
+          tc_fence_before();
+          mbar_arrive(smem_u32(&s_fb[2]));  // (the item's publish below releases the red.adds)
+        }
         wrote = final;
         lm_last_check = epi == kEpArgmax;
       } else if (kind == kKEmbed) {
@@ -1297,7 +1428,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           asm_->last = staged;
         }
         if (tid == 0) {
-          if (a.fine) {  // this head group's QKV tiles only (group-blocked: consecutive tiles)
+          if (fine_for(a, kKAttn)) {  // this head group's QKV tiles only (group-blocked: consecutive tiles)
             const int tpg = (G + 2) * HD / BM;
             wait_tiles(flags_of(kGQkv), gh * tpg, (gh + 1) * tpg, stamp(layer));
           } else if (p - 1 > attn_dep_ok) {
@@ -1337,7 +1468,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
             }
           }
         } else if (wrote) {
-          if (!a.fine) {
+          if (!fine_for(a, kind_of(p + 1, a.L))) {  // the consumer phase waits phase-level
           } else if (is_gemm(kind)) {  // tile final: stamp it for the fine-grained consumers
             const int gk = gemm_of(kind);
             const int t = j % a.g[gk].ntiles;
@@ -1365,7 +1496,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
   __syncthreads();
   if (warp == kWarpMma0) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols));
   }
   if (threadIdx.x == 0) {
     __threadfence();
@@ -1517,10 +1648,15 @@ bool build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_f
   // fine-grained dependencies).  O and down first: their tile counts (d / 128) are the same on
   // every tensor-parallel rank, so their regions sit at the same offsets in every rank's
   // workspace -- the peers' red.adds target them.
+  // Fused gate/up -> down (FwArgs::fuse): small models only -- the 16-column accumulators of
+  // every down output tile must fit the 256 spare TMEM columns, and only the hd 64 instances
+  // are compiled with it.
+  const bool fuse = m.fuse && m.tp <= 1 && m.hd == 64 && (m.H / m.KV == 2 || m.H / m.KV == 4) &&
+                    (m.d / BM) % kUPS == 0 && (m.d / BM) * BN <= 256;
   auto place_ws = [&](GemmKind& g) {
     g.ws_off = ws;
     g.cnt_off = cnt;
-    if (g.nchunks > 1 || g.xr) ws += (long long)g.ntiles * BM * BN;
+    if (g.nchunks > 1 || g.xr || (fuse && &g == &a->g[kGDown])) ws += (long long)g.ntiles * BM * BN;
     cnt += g.ntiles * kCounterInts;
   };
   const uint8_t* w0 = m.wt_layer0;
@@ -1539,6 +1675,12 @@ bool build_kinds(const ModelView& m, int units_per_item, FwArgs* a, size_t* ws_f
   a->g[kGDown].gnext = m.norms + 2 * m.d;   // attention RMSNorm of layer l+1 at 2l+2 (final norm at 2L)
   a->g[kGDown].gnext_stride = 2 * m.d;
   a->g[kGLm] = kind(kEpArgmax, 0, m.vocab / BM, m.d, m.vocab, m.vocab, m.wt_lm, 0, "LM");
+  a->fuse = fuse;
+  if (fuse) {  // down: one weight-less merge item per output tile (gate/up keeps its chunking;
+               // its merging chunks carry the down slabs)
+    GemmKind& g = a->g[kGDown];
+    g.kc = g.kb; g.nchunks = 1; g.nitems = g.ntiles; g.nchunks_total = 1;
+  }
   if (m.tp > 1) {
     for (int k : {kGO, kGDown, kGQkv, kGGu, kGLm}) place_ws(a->g[k]);
   } else {  // unsharded: construction order
@@ -1571,15 +1713,15 @@ int forward_smem_bytes(int stages, int hd, int group) {
   return 1024 + stages * (kStageW + kStageX) + sc + ((ctl + 127) & ~127);
 }
 
-template <int HD, int G, int MINB, bool TP>
+template <int HD, int G, int MINB, bool TP, bool FUSE = false>
 static cudaError_t launch_m(const FwArgs& a, const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& m2,
                             const CUtensorMap& m3, int grid, int stages, cudaStream_t st) {
   const int smem = forward_smem_bytes(stages, HD, G);
   static SmemOptIn opt;  // per device (one process may hold models on two GPUs)
-  if (cudaError_t e = opt.ensure(k_forward<HD, G, MINB, TP>, smem)) return e;
+  if (cudaError_t e = opt.ensure(k_forward<HD, G, MINB, TP, FUSE>, smem)) return e;
   FwArgs b = a;
   b.stages = stages;
-  k_forward<HD, G, MINB, TP><<<grid, kThreads, smem, st>>>(m0, m1, m2, m3, b);
+  k_forward<HD, G, MINB, TP, FUSE><<<grid, kThreads, smem, st>>>(m0, m1, m2, m3, b);
   return cudaGetLastError();
 }
 
@@ -1589,6 +1731,9 @@ template <int HD, int G>
 static cudaError_t launch_t(const FwArgs& a, const CUtensorMap& m0, const CUtensorMap& m1, const CUtensorMap& m2,
                             const CUtensorMap& m3, int grid, int stages, cudaStream_t st) {
   if (a.tp > 1) return launch_m<HD, G, 1, true>(a, m0, m1, m2, m3, grid, stages, st);
+  if constexpr (HD == 64 && (G == 2 || G == 4)) {
+    if (a.fuse) return launch_m<HD, G, 1, false, true>(a, m0, m1, m2, m3, grid, stages, st);  // 512 TMEM columns
+  }
   if (forward_smem_bytes(stages, HD, G) <= 232448 / 2 - 1024)
     return launch_m<HD, G, 2, false>(a, m0, m1, m2, m3, grid, stages, st);
   return launch_m<HD, G, 1, false>(a, m0, m1, m2, m3, grid, stages, st);

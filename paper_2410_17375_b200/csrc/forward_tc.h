@@ -86,7 +86,15 @@ struct FwArgs {
   size_t qo_bytes;              // QKV + O tiled weight bytes of one layer (contiguous)
   int inflight;                 // max unlanded weight units per CTA (0 = ring depth)
   int debug;                    // perf-isolation bits (AMUSD_FW_DEBUG), 0 in production
-  int fine;                     // 1: per-tile dependencies (AMUSD_FW_FINE); 0: phase-level (default)
+  // Fused gate/up -> down (AMUSD_FW_FUSE, small models): every gate/up item is a whole tile (64
+  // features); after its SiLU*up epilogue the same CTA streams the down weights of exactly those
+  // 64 features (one 16 KB unit per output tile), multiplies them by the fresh act tile and
+  // red.adds the int64 partials into the down accumulators.  The down phase shrinks to one
+  // weight-less item per output tile that waits for all gate/up contributions and runs the
+  // residual epilogue: one dependent GEMM phase less per layer.
+  int fuse;
+  int fine;                     // AMUSD_FW_FINE: bit (1 << consumer kind) = per-tile dependencies for
+                                // that kind; 0 = phase-level everywhere (default)
   // Draft cut (co-located / split AMUSD draft only, else null): once the verifier has raised
   // a rollback request (*ab_req != ctl->rb_ack_local) or completion (*ab_done), this forward's
   // token will be discarded (k_draft_end), so the grab counter is moved past the item list.
@@ -133,6 +141,7 @@ struct ModelView {
   float* ssp;
   float* sspb;
   __nv_bfloat16* act_b;
+  int fuse;                     // 1: gate/up -> down fused (FwArgs::fuse); build_kinds clears it where unsupported
 };
 // ws_floats: int64 accumulator regions of all kinds (in float units); cnt_ints: tile counters;
 // max_tiles: largest producer tile count (flag region size).
