@@ -110,18 +110,19 @@ def test_reference_engines_over_decoder(ref_pair):
     Dec, Coin, Shim = make_models(S)
     prompt = [(31 * i + 7) % 4000 + 3 for i in range(16)]
     n = 24
-    cfg = S.DecodeConfig(max_new_tokens=n, draft_window_k=4)
+    # bounded lead: the coin draft follows the canonical path only as far as `canon` reaches,
+    # so the draft (<= verified + lead) must never outrun it (rho = 1 -> zero rollbacks)
+    cfg = S.DecodeConfig(max_new_tokens=n, draft_window_k=4, max_draft_lead=32)
     verify = Dec(rv)
     ar = S.decode_autoregressive(verify, prompt, cfg)
     assert len(ar.tokens) == n and ar.finished_by == "length_limit"
-    canon = list(prompt) + S.decode_autoregressive(verify, prompt, S.DecodeConfig(max_new_tokens=n + 16)).tokens
+    canon = list(prompt) + S.decode_autoregressive(verify, prompt, S.DecodeConfig(max_new_tokens=n + 72)).tokens
     assert canon[len(prompt):len(prompt) + n] == ar.tokens
     for rho in (0.0, 0.8, 1.0):
         draft = Coin(rd, canon, rho, 1234)
         sy = S.decode_speculative_sync(draft, verify, prompt, cfg)
-        # the reference ThreadExecutor runs real threads; under a loaded host the suite has seen a
-        # rare IndexError from inside a run (timing-dependent, not reproducible in isolation):
-        # retry, keeping the traceback for the final failure
+        # the reference ThreadExecutor runs real threads: retry a run that raises, keeping the
+        # traceback for the final failure
         errs = []
         for _ in range(3):
             ex = Shim()
@@ -137,6 +138,7 @@ def test_reference_engines_over_decoder(ref_pair):
         asy.trace.validate()
         # rollback-count theorem (pkg/tests/test_engines.py:293-321) along the canonical path
         verified = max(e.pos_hi for e in asy.trace.events if e.kind.startswith("verify_")) - len(prompt)
+        assert verified <= len(canon) - len(prompt), verified
         dis = [i for i in range(verified)
                if draft.next_token(_advanced(draft, prompt, canon, i)) != canon[len(prompt) + i]]
         assert asy.stats.rollbacks == len(dis), rho
