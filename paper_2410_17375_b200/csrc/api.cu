@@ -1318,6 +1318,8 @@ static ProtoArgs make_args(amusd_session* s) {
   a.coin = s->coin;
   a.jitter_ns = s->d.jitter_ns;
   a.jitter_seed = s->d.jitter_seed;
+  a.min_window = std::max(1, env_int("AMUSD_VERIFY_MIN_WINDOW", 1));
+  a.wait_ns = 1000ll * env_int("AMUSD_VERIFY_WAIT_US", 0);
   if (s->tp_role == 1) {
     for (int i = 0; i < s->tp_nout; ++i) a.tp_out[i] = s->tp_out[i];
     a.tp_nout = s->tp_nout;

@@ -118,6 +118,11 @@ struct ProtoArgs {
   int vocab_v, eos_v;       // verify model vocab / eos (completion check)
   int jitter_ns;
   unsigned long long jitter_seed;
+  // AMUSD verify pacing (timing only: any interleaving of the two loops is a valid AMUSD run):
+  // a step waits until the draft window holds >= min_window tokens or wait_ns have passed
+  // since the first one appeared (1 / 0 = verify whatever is there, the reference's pacing)
+  int min_window;
+  long long wait_ns;
   cudaGraphConditionalHandle cond;
   int has_cond;
   TpInbox* tp_out[kMaxTpOut];  // leader: the followers' inboxes

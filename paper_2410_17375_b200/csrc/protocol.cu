@@ -218,6 +218,7 @@ __global__ void k_verify_begin(ProtoArgs a) {
   if (L != R) L->vb.iters = R->vb.iters;
   jitter(a, 0x5E, *a.vtrace.count);
   const long long t_enter = globaltimer();
+  long long t_first = 0;
   int pd;
   for (;;) {
     if (ld_volatile(&L->db.error)) {  // draft-side violation: end the run
@@ -229,7 +230,12 @@ __global__ void k_verify_begin(ProtoArgs a) {
     }
     if (ld_acquire(&L->db.rb_ack) == c->rb_ack_local) {
       pd = ld_acquire(&L->db.p_d);
-      if (pd > s->len) break;
+      if (pd > s->len) {
+        if (pd - s->len >= a.min_window) break;
+        const long long now = globaltimer();
+        if (!t_first) t_first = now;
+        else if (now - t_first >= a.wait_ns) break;
+      }
     }
     if (globaltimer() - t_enter > kSpinTimeoutNs) {
       mb_write_both(&R->vb.error, &L->vb.error, kErrTimeout);
