@@ -184,3 +184,22 @@ def test_full_agreement_no_rollbacks():
     assert res.stats.rollbacks == 0 and res.stats.wasted_draft_tokens == 0
     sy = P.decode_speculative_sync(d, v, [1, 2, 3], P.DecodeConfig(max_new_tokens=10, draft_window_k=4))
     assert sy.stats.verify_steps == 2 and sy.stats.accepted_per_verify_step == 5.0
+
+
+@pytest.mark.parametrize("minw,wait_us", [(3, 200), (8, 50), (4, 20000)])
+def test_verify_pacing_keeps_tokens(monkeypatch, minw, wait_us):
+    """AMUSD_VERIFY_MIN_WINDOW / _WAIT_US change only when the verify loop starts a step: tokens
+    stay the AR tokens, traces validate, and a step never waits forever (a window the draft cannot fill -- lead cap 2 < min window -- ends by the
+    time bound)."""
+    monkeypatch.setenv("AMUSD_VERIFY_MIN_WINDOW", str(minw))
+    monkeypatch.setenv("AMUSD_VERIFY_WAIT_US", str(wait_us))
+    P.engines.clear_sessions()  # the pacing is read when a session's graphs are built
+    try:
+        for seed, rho, lead in ((31, 0.7, None), (32, 0.9, 2), (33, 0.0, None)):
+            d, v = _pair(seed, rho, 997, 0, True, max_seq=256)
+            cfg = P.DecodeConfig(max_new_tokens=60, max_draft_lead=lead)
+            res = P.decode_speculative_async(d, v, [1, 2, 3, 4], cfg)
+            assert res.tokens == O.decode_ar(O.ChainOracle(seed, 997, 0, True), [1, 2, 3, 4], 60)[0], seed
+            res.trace.validate()
+    finally:
+        P.engines.clear_sessions()
